@@ -155,7 +155,10 @@ struct Oracle {
       if (c > 0 && !(t[c - 1] < t[c] || (t[c - 1] == t[c] && sess[c - 1] < sess[c]))) return 6;
       if (sess[c] >= n_sessions || vnode[c] >= n_aeg) return 7;
       if (prompt[c] < 1 || newt[c] > prompt[c]) return 8;
-      if (roff[c + 1] < roff[c]) return 9;
+      if (roff[c + 1] <= roff[c]) return 9;   // every call touches >= 1 range
+      int64_t work = (int64_t(prompt[c]) * 1000000 + pc.prefill_tok_s - 1) / pc.prefill_tok_s +
+                     (int64_t(outt[c]) * 1000000 + pc.decode_tok_s - 1) / pc.decode_tok_s;
+      if (work >= (int64_t(1) << 32)) return 23;   // a call's work must fit 32 bits
     }
     std::vector<std::pair<uint64_t, uint64_t>> spans;
     for (uint32_t a = 0; a < n_types; ++a) {
@@ -270,7 +273,7 @@ struct Oracle {
           else keep.push_back(q);
         }
         Q[v].swap(keep);
-        if (!fin[s]) { cnt[v][styp[s]]--; cnt[th][styp[s]]++; }
+        if (!fin[s]) { cnt[aff[s]][styp[s]]--; cnt[th][styp[s]]++; }   // s counted at its affinity node
         aff[s] = int32_t(th); moved[s] = 1; idle[th] = 0;
         migs.push_back({uint32_t(e), uint32_t(s), v, th});
         got[th] = 1;
@@ -671,9 +674,9 @@ Oracle* build(const ODesc* d, const OPlace* p, int* err) {
   o->term = cp(d->node_terminal, d->n_aeg_nodes); o->tlo = cp(d->type_shared_lo, d->n_types);
   o->tlen = cp(d->type_shared_len, d->n_types);
   o->pc = *p;
+  if (p->epoch_us <= 0 || p->kappa == 0 || p->prefill_tok_s == 0 || p->decode_tok_s == 0) { *err = 100; delete o; return nullptr; }
   int v = o->validate();
   if (v) { *err = v; delete o; return nullptr; }
-  if (p->epoch_us <= 0 || p->kappa == 0 || p->prefill_tok_s == 0 || p->decode_tok_s == 0) { *err = 100; delete o; return nullptr; }
   o->owner.assign(o->n_blocks, 0xFFFFFFFFu);
   for (uint32_t a = 0; a < o->n_types; ++a)
     for (uint32_t i = 0; i < o->tlen[a]; ++i) o->owner[o->tlo[a] + i] = o->n_sessions + a;

@@ -1,0 +1,121 @@
+// Block-level building blocks shared by the replay (A7) and the bulk select (A6) kernels:
+// reductions, an exclusive scan, and radix select of the k largest unique uint64 keys.
+#pragma once
+#include "saga_internal.cuh"
+
+namespace saga {
+
+struct Add { template <class T> __device__ T operator()(T a, T b) const { return a + b; } };
+struct Max { template <class T> __device__ T operator()(T a, T b) const { return a > b ? a : b; } };
+struct Or { template <class T> __device__ T operator()(T a, T b) const { return a | b; } };
+struct And { template <class T> __device__ T operator()(T a, T b) const { return a & b; } };
+
+template <int BT>
+struct BlockScratch {
+  uint32_t u32[BT / 32];
+  unsigned long long u64[BT / 32];
+  long long i64[BT / 32];
+  uint32_t hist[256];
+  uint32_t sel_d, sel_above;
+};
+
+template <int BT, class T, class Op>
+__device__ __forceinline__ T block_reduce(T x, Op op, T* scratch /*[BT/32]*/) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
+  if (lane == 0) scratch[wid] = x;
+  __syncthreads();
+  T r = scratch[0];
+#pragma unroll
+  for (int w = 1; w < BT / 32; ++w) r = op(r, scratch[w]);
+  __syncthreads();
+  return r;
+}
+
+// exclusive scan of one value per thread; *total receives the block sum
+template <int BT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* scratch /*[BT/32]*/) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  uint32_t pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < BT / 32; ++w) { uint32_t s = scratch[w]; if (w < wid) pre += s; tot += s; }
+  __syncthreads();
+  *total = tot;
+  return pre + x - v;
+}
+
+// Threshold T with #{i : kb[i] >= T} == k for n unique keys and 1 <= k <= n.
+// Radix select from the highest bit on which the keys differ, 8-bit digits, early exit when the
+// pivot bucket is consumed exactly.  Every pass re-reads kb (L2-resident for replay sizes).
+template <int BT>
+__device__ uint64_t radix_select(const uint64_t* kb, uint32_t n, uint32_t k, BlockScratch<BT>& sm) {
+  unsigned long long o = 0, an = ~0ull;
+  for (uint32_t i = threadIdx.x; i < n; i += BT) { const uint64_t x = kb[i]; o |= x; an &= x; }
+  o = block_reduce<BT, unsigned long long>(o, Or(), sm.u64);
+  an = block_reduce<BT, unsigned long long>(an, And(), sm.u64);
+  const unsigned long long diff = o ^ an;
+  if (diff == 0) return o;
+  const int top = 63 - __clzll(diff);
+  const uint64_t above_mask = (top == 63) ? 0ull : ~((2ull << top) - 1ull);
+  uint64_t prefix = an & above_mask;   // bits above `top` are common to every key
+  uint64_t mask = above_mask;
+  int width = min(8, top + 1);
+  int shift = top + 1 - width;
+  uint32_t rem = k;
+  while (true) {
+    for (int i = threadIdx.x; i < 256; i += BT) sm.hist[i] = 0;
+    __syncthreads();
+    const uint32_t dm = (1u << width) - 1u;
+    for (uint32_t i = threadIdx.x; i < n; i += BT) {
+      const uint64_t x = kb[i];
+      if ((x & mask) == prefix) atomicAdd(&sm.hist[(uint32_t)(x >> shift) & dm], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint32_t local[8];
+      uint32_t s = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { local[j] = sm.hist[255 - (lane * 8 + j)]; s += local[j]; }
+      uint32_t x = s;
+#pragma unroll
+      for (int of = 1; of < 32; of <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, of);
+        if (lane >= of) x += y;
+      }
+      uint32_t above = x - s;  // keys in digits above this lane's first digit
+      int found = -1;
+      uint32_t above_d = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (found < 0 && above < rem && rem <= above + local[j]) { found = 255 - (lane * 8 + j); above_d = above; }
+        above += local[j];
+      }
+      const uint32_t fm = __ballot_sync(0xffffffffu, found >= 0);
+      const int src = __ffs(fm) - 1;
+      const int d = __shfl_sync(0xffffffffu, found, src);
+      const uint32_t ab = __shfl_sync(0xffffffffu, above_d, src);
+      if (lane == 0) { sm.sel_d = (uint32_t)d; sm.sel_above = ab; }
+    }
+    __syncthreads();
+    const uint32_t d = sm.sel_d, ab = sm.sel_above, hd = sm.hist[d];
+    __syncthreads();
+    rem -= ab;
+    prefix |= (uint64_t)d << shift;
+    mask |= (uint64_t)dm << shift;
+    if (hd == rem || shift == 0) return prefix;
+    width = min(8, shift);
+    shift -= width;
+  }
+}
+
+}  // namespace saga

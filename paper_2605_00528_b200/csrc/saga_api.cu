@@ -1,0 +1,262 @@
+// C ABI of libsaga (include/saga.h): argument checks, handle lifetime, stream ordering.
+// Every compute step runs in the kernels of k_*.cu; nothing here touches trace data on the host.
+#include <cstring>
+#include <mutex>
+
+#include "saga_internal.cuh"
+
+namespace saga {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+static void mempool_setup(int device) {
+  static std::mutex mu;
+  static uint64_t done_mask = 0;
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 64 && (done_mask >> device) & 1ull) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool across steps
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (device < 64) done_mask |= 1ull << device;
+}
+
+}  // namespace saga
+
+using namespace saga;
+
+#define CHECK_HANDLE(t)                                                        \
+  do {                                                                         \
+    if (!(t)) { set_error("%s: NULL handle", __func__); return SAGA_ERR_INVALID_ARG; } \
+    if ((t)->sticky_error) { set_error("%s: handle is in a CUDA error state", __func__); return SAGA_ERR_CUDA; } \
+  } while (0)
+
+#define GUARD(t, call)                                 \
+  do {                                                 \
+    saga_status _s = (call);                           \
+    if (_s == SAGA_ERR_CUDA && (t)) (t)->sticky_error = true; \
+    if (_s != SAGA_OK) return _s;                      \
+  } while (0)
+
+extern "C" {
+
+const char* saga_last_error(void) { return g_err.c_str(); }
+
+uint64_t saga_kernel_launches(void) { return g_launches.load(); }
+
+void saga_free_trace(saga_trace* t) {
+  if (!t) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(t->device);
+  for (void* p : t->allocs) cudaFreeAsync(p, t->stream);
+  cudaStreamSynchronize(t->stream);
+  cudaSetDevice(prev);
+  delete t;
+}
+
+saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask, int device,
+                            saga_stream_t stream, saga_trace** out) {
+  g_err.clear();
+  if (!desc || !cfg || !out) { set_error("saga_load_trace: NULL argument"); return SAGA_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (cfg->epoch_us <= 0 || cfg->kappa == 0 || cfg->prefill_tok_s == 0 || cfg->decode_tok_s == 0) {
+    set_error("saga_load_trace: epoch_us, kappa, prefill_tok_s and decode_tok_s must be positive");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    set_error("saga_load_trace: no CUDA device %d", device);
+    return SAGA_ERR_INVALID_ARG;
+  }
+  SAGA_CK(cudaSetDevice(device));
+  mempool_setup(device);
+  saga_trace* t = new saga_trace();
+  t->device = device;
+  t->stream = (cudaStream_t)stream;
+  t->pcfg = *cfg;
+  t->n_calls = desc->n_calls;
+  t->n_sessions = desc->n_sessions;
+  t->n_types = desc->n_types;
+  t->n_nodes = desc->n_nodes;
+  saga_status st = load_validate_and_derive(t, desc);
+  if (st != SAGA_OK) { saga_free_trace(t); return st; }
+  t->owned_mask = owned_node_mask ? owned_node_mask : (desc->n_nodes >= 32 ? 0xFFFFFFFFu : ((1u << desc->n_nodes) - 1u));
+  t->nodes.assign(desc->n_nodes, NodeDev());
+  st = run_placement(t);
+  if (st != SAGA_OK) { saga_free_trace(t); return st; }
+  for (uint32_t w = 0; w < desc->n_nodes; ++w) {
+    if (!((t->owned_mask >> w) & 1u)) continue;
+    t->nodes[w].owned = true;
+    st = run_expand(t, w);
+    if (st != SAGA_OK) { saga_free_trace(t); return st; }
+  }
+  cudaError_t e = cudaStreamSynchronize(t->stream);
+  if (e != cudaSuccess) {
+    set_error("saga_load_trace: %s", cudaGetErrorString(e));
+    saga_free_trace(t);
+    return SAGA_ERR_CUDA;
+  }
+  *out = t;
+  return SAGA_OK;
+}
+
+saga_status saga_trace_info(const saga_trace* t, uint32_t node, uint64_t* n_access, uint32_t* n_local_blocks) {
+  CHECK_HANDLE(t);
+  if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_trace_info: node %u not owned", node); return SAGA_ERR_STATE; }
+  const NodeDev& nd = t->nodes[node];
+  if (n_access) *n_access = nd.N;
+  if (n_local_blocks) *n_local_blocks = nd.nu_done ? nd.n_local : UINT32_MAX;
+  return SAGA_OK;
+}
+
+saga_status saga_placement(const saga_trace* t, uint8_t* node_host, uint32_t* mig_host, uint64_t mig_cap, int64_t* stats) {
+  CHECK_HANDLE(t);
+  SAGA_CK(cudaSetDevice(t->device));
+  if (node_host) SAGA_CK(cudaMemcpyAsync(node_host, t->node_of, t->n_calls, cudaMemcpyDeviceToHost, t->stream));
+  if (mig_host && mig_cap) {
+    uint64_t n = std::min<uint64_t>(mig_cap, t->n_mig);
+    if (n) SAGA_CK(cudaMemcpyAsync(mig_host, t->migs, n * sizeof(Mig), cudaMemcpyDeviceToHost, t->stream));
+  }
+  SAGA_CK(cudaStreamSynchronize(t->stream));
+  if (stats) { stats[0] = t->n_steals; stats[1] = t->n_reroutes; stats[2] = t->n_mig; }
+  return SAGA_OK;
+}
+
+saga_status saga_node_stream_sizes(const saga_trace* t, uint32_t node, uint64_t* n_access, uint32_t* n_events,
+                                   uint32_t* n_groups, uint32_t* n_inv) {
+  CHECK_HANDLE(t);
+  if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("node %u not owned", node); return SAGA_ERR_STATE; }
+  const NodeDev& nd = t->nodes[node];
+  if (n_access) *n_access = nd.N;
+  if (n_events) *n_events = nd.J;
+  if (n_groups) *n_groups = nd.G;
+  if (n_inv) *n_inv = nd.n_inv;
+  return SAGA_OK;
+}
+
+namespace {
+// internal work of a handle is ordered on its own stream; callers' streams are joined with events
+saga_status join(cudaStream_t from, cudaStream_t to) {
+  if (!from || !to || from == to) return SAGA_OK;
+  cudaEvent_t ev;
+  SAGA_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  SAGA_CK(cudaEventRecord(ev, from));
+  SAGA_CK(cudaStreamWaitEvent(to, ev, 0));
+  cudaEventDestroy(ev);
+  return SAGA_OK;
+}
+__global__ void k_pack_ev(const uint32_t* ev_e, const uint32_t* ev_g, uint32_t J, uint32_t* out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < J; j += gridDim.x * blockDim.x) {
+    out[3 * j] = ev_e[j];
+    out[3 * j + 1] = ev_g[j];
+    out[3 * j + 2] = ev_g[j + 1] - ev_g[j];
+  }
+}
+__global__ void k_pack_grp(const uint64_t* g_pos, const uint32_t* g_kind, uint32_t G, uint64_t* out) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+    out[2 * g] = g_pos[g];
+    out[2 * g + 1] = g_kind[g];
+  }
+}
+}  // namespace
+
+saga_status saga_node_stream(const saga_trace* t, uint32_t node, uint32_t* block_dev, uint32_t* ev_dev, uint64_t* grp_dev,
+                             int64_t* grp_t_dev, uint32_t* inv_dev, saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("node %u not owned", node); return SAGA_ERR_STATE; }
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(const_cast<saga_trace*>(t), join(t->stream, (cudaStream_t)stream));
+  cudaStream_t s = stream ? (cudaStream_t)stream : t->stream;
+  const NodeDev& nd = t->nodes[node];
+  if (block_dev && nd.N) SAGA_CK(cudaMemcpyAsync(block_dev, nd.block, nd.N * 4, cudaMemcpyDeviceToDevice, s));
+  if (ev_dev && nd.J) { k_pack_ev<<<(nd.J + 255) / 256, 256, 0, s>>>(nd.ev_e, nd.ev_g, nd.J, ev_dev); count_launch(); }
+  if (grp_dev && nd.G) { k_pack_grp<<<(nd.G + 255) / 256, 256, 0, s>>>(nd.g_pos, nd.g_kind, nd.G, grp_dev); count_launch(); }
+  if (grp_t_dev && nd.G) SAGA_CK(cudaMemcpyAsync(grp_t_dev, nd.g_t, size_t(nd.G) * 8, cudaMemcpyDeviceToDevice, s));
+  if (inv_dev && nd.n_inv) SAGA_CK(cudaMemcpyAsync(inv_dev, nd.inv_s, size_t(nd.n_inv) * 4, cudaMemcpyDeviceToDevice, s));
+  SAGA_CK_LAUNCH();
+  return SAGA_OK;
+}
+
+saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_use_dev, uint32_t* local_id_dev,
+                                 saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_belady_next_use: node %u not owned", node); return SAGA_ERR_STATE; }
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(t, join((cudaStream_t)stream, t->stream));
+  GUARD(t, run_next_use(t, node, next_use_dev, local_id_dev, t->stream));
+  GUARD(t, join(t->stream, (cudaStream_t)stream));
+  return SAGA_OK;
+}
+
+saga_status saga_sweep_range(const saga_trace* t, uint32_t node, uint32_t* w_lo, uint32_t* w_hi) {
+  CHECK_HANDLE(t);
+  if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_sweep_range: node %u not owned", node); return SAGA_ERR_STATE; }
+  const NodeDev& nd = t->nodes[node];
+  if (!nd.nu_done) { set_error("saga_sweep_range: call saga_belady_next_use(node %u) first", node); return SAGA_ERR_STATE; }
+  if (w_lo) *w_lo = nd.w_lo;
+  if (w_hi) *w_hi = nd.w_hi;
+  return SAGA_OK;
+}
+
+saga_status saga_aeg_score(const saga_trace* t, const saga_score_batch* batch, const saga_replay_cfg* cfg, float* score_dev,
+                           uint64_t* key_dev, saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if (!batch || !cfg || !key_dev) { set_error("saga_aeg_score: NULL argument"); return SAGA_ERR_INVALID_ARG; }
+  if (batch->policy != SAGA_POLICY_AEG && batch->policy != SAGA_POLICY_BELADY) {
+    set_error("saga_aeg_score: policy must be AEG or BELADY");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  if (batch->policy == SAGA_POLICY_AEG)
+    for (uint32_t w = 0; w < t->n_nodes; ++w)
+      if (t->nodes[w].owned && !t->nodes[w].nu_done) {
+        set_error("saga_aeg_score: saga_belady_next_use(node %u) must run first", w);
+        return SAGA_ERR_STATE;
+      }
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(const_cast<saga_trace*>(t), join(t->stream, (cudaStream_t)stream));
+  GUARD(const_cast<saga_trace*>(t), run_score(t, batch, cfg, score_dev, key_dev, stream ? (cudaStream_t)stream : t->stream));
+  return SAGA_OK;
+}
+
+saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_dev, const uint32_t* k_dev, uint32_t n_seg,
+                              const uint64_t* out_off_dev, uint32_t* victim_idx_dev, saga_stream_t stream) {
+  g_err.clear();
+  if (n_seg && (!key_dev || !seg_off_dev || !k_dev || !out_off_dev || !victim_idx_dev)) {
+    set_error("saga_evict_select: NULL argument");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  return run_select(key_dev, seg_off_dev, k_dev, n_seg, out_off_dev, victim_idx_dev, (cudaStream_t)stream);
+}
+
+saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
+                        const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if (!cfg || (n_caps && !caps) || (n_owned && !nodes) || !counters_dev) { set_error("saga_replay: NULL argument"); return SAGA_ERR_INVALID_ARG; }
+  if ((cfg->policy_mask & ~7u) || !(cfg->policy_mask & 7u)) { set_error("saga_replay: bad policy_mask"); return SAGA_ERR_INVALID_ARG; }
+  if (cfg->p_high_pm <= cfg->p_low_pm || cfg->p_high_pm > 1000) { set_error("saga_replay: need p_low_pm < p_high_pm <= 1000"); return SAGA_ERR_INVALID_ARG; }
+  for (uint32_t i = 0; i < n_caps; ++i)
+    if (caps[i] == 0 || caps[i] > (1u << 28)) { set_error("saga_replay: capacity %u out of range (1..2^28)", caps[i]); return SAGA_ERR_CAPACITY; }
+  for (uint32_t i = 0; i < n_owned; ++i) {
+    if (nodes[i] >= t->n_nodes || !t->nodes[nodes[i]].owned) { set_error("saga_replay: node %u not owned", nodes[i]); return SAGA_ERR_STATE; }
+    if (!t->nodes[nodes[i]].nu_done) { set_error("saga_replay: saga_belady_next_use(node %u) must run first", nodes[i]); return SAGA_ERR_STATE; }
+  }
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(t, join((cudaStream_t)stream, t->stream));
+  GUARD(t, run_replay(t, cfg, caps, n_caps, nodes, n_owned, counters_dev, t->stream));
+  GUARD(t, join(t->stream, (cudaStream_t)stream));
+  return SAGA_OK;
+}
+
+}  // extern "C"

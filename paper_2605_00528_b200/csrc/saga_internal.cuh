@@ -1,0 +1,230 @@
+// Internal declarations of libsaga (B200 / sm_100a).  Not part of the ABI (see include/saga.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "saga.h"
+
+namespace saga {
+
+constexpr uint32_t INF32 = 0xFFFFFFFFu;
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+// packed per-position word of a node stream after next-use: local id | flags
+constexpr uint32_t LID_FTN = 1u << 31;   // first touch of the block at this node
+constexpr uint32_t LID_NFIE = 1u << 30;  // NOT the first record of the block in its epoch
+constexpr uint32_t LID_MASK = (1u << 30) - 1;
+constexpr int NTHREADS = 256;
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void set_error(const char* fmt, ...);
+
+struct Mig { uint32_t e, s, v, t; };
+struct ActRec { uint32_t e, w, mask, pad; };
+
+// ------------------------------------------------------------------------------------------
+// device-side view of the trace (all pointers device memory)
+// ------------------------------------------------------------------------------------------
+struct TraceView {
+  uint32_t n_calls, n_sessions, n_types, n_aeg, n_edges, n_ranges, n_blocks, n_nodes, btok;
+  int64_t epoch_us;
+  uint32_t prefill_tok_s, decode_tok_s;
+  const int64_t* call_t;
+  const uint32_t* call_sess;
+  const uint32_t* call_v;
+  const uint32_t* call_prompt;
+  const uint32_t* call_out;
+  const uint32_t* call_new;
+  const uint8_t* call_last;
+  const uint32_t* roff;
+  const uint32_t* rlo;
+  const uint32_t* rlen;
+  const uint16_t* styp;
+  const uint32_t* slo;
+  const uint32_t* slen;
+  const uint32_t* eoff;
+  const uint32_t* edst;
+  const float* ep;
+  const uint32_t* eq16;
+  const int64_t* ttl;
+  const uint32_t* obs;
+  const uint8_t* term;
+  const uint32_t* tlo;
+  const uint32_t* tlen;
+  // derived (A1)
+  const uint32_t* ecall;   // admission epoch e(c) = t/E + 1
+  const int64_t* tend;     // tool start t_c + prefill(new) + decode(out)
+  const uint64_t* rsum;    // blocks accessed by the call
+  const uint32_t* owner;   // [n_blocks] session, or n_sessions + type, or NONE
+  const uint32_t* sc_off;  // [n_sessions+1] calls of each session (CSR, ascending)
+  const uint32_t* sc_call;
+  const float* ci_P;       // P_reuse(s) after call c (eq:reuse + eq:overlap), fp32 pinned
+  const uint32_t* ci_size; // size(s) after call c in blocks (eq:size numerator)
+  const uint8_t* ci_fin;   // is_last or terminal
+};
+
+struct NodeDev {
+  bool owned = false;
+  uint64_t N = 0;          // accesses
+  uint32_t J = 0;          // events incl. the trailing sentinel
+  uint32_t G = 0;          // record groups
+  uint32_t n_inv = 0;
+  uint32_t* block = nullptr;
+  uint64_t* g_pos = nullptr;   // [G+1]
+  int64_t* g_t = nullptr;      // [G]
+  uint32_t* g_call = nullptr;  // [G]
+  uint32_t* g_kind = nullptr;  // [G] 0 CALL, 1 MIG
+  uint32_t* g_e = nullptr;     // [G]
+  uint32_t* ev_e = nullptr;    // [J]
+  uint32_t* ev_g = nullptr;    // [J+1]
+  uint32_t* ev_inv = nullptr;  // [J+1]
+  uint32_t* ev_act = nullptr;  // [J]
+  uint32_t* inv_s = nullptr;   // [n_inv]
+  uint32_t* inv_e = nullptr;   // [n_inv]
+  // A4 products
+  bool nu_done = false;
+  uint32_t n_local = 0, w_lo = 0, w_hi = 0;
+  uint32_t* lidf = nullptr;    // [N] local id | LID_FTN | LID_NFIE
+  uint32_t* nxt = nullptr;     // [N] next use
+  uint32_t* lown = nullptr;    // [n_local] owner of the local block
+  uint32_t n_upd = 0;
+  uint32_t* upd_c = nullptr;   // calls of sessions present at the node (call order)
+};
+
+}  // namespace saga
+
+struct saga_trace {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool sticky_error = false;
+  saga_place_cfg pcfg{};
+  uint32_t owned_mask = 0;
+  saga::TraceView v{};
+  // host metadata
+  uint32_t n_calls = 0, n_sessions = 0, n_types = 0, n_nodes = 0;
+  // placement outputs
+  uint8_t* node_of = nullptr;       // [n_calls]
+  saga::Mig* migs = nullptr;        // [n_mig]
+  saga::ActRec* act = nullptr;      // [n_act]
+  uint32_t n_mig = 0, n_act = 0;
+  int64_t n_steals = 0, n_reroutes = 0;
+  std::vector<saga::NodeDev> nodes;
+  std::vector<void*> allocs;        // every device allocation owned by the handle
+};
+
+namespace saga {
+
+template <class T>
+T* dalloc(saga_trace* t, size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  if (cudaMallocAsync(&p, n * sizeof(T), t->stream) != cudaSuccess) return nullptr;
+  t->allocs.push_back(p);
+  return static_cast<T*>(p);
+}
+
+// ------------------------------------------------------------------------------------------
+// device helpers shared by the kernels of the CUDA path (not by the oracle)
+// ------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Per-owner inputs of the WA-LRU key at boundary T_e (resolved by the caller).
+struct OwnerKeyIn {
+  uint32_t size;     // blocks (eq:size numerator)
+  float P;           // P_reuse (eq:reuse), already 0 for finished sessions, act for shared
+  bool prot_shared;  // shared prefix: protected iff act
+  bool shared;
+  bool fin;
+  int64_t t_call;    // tool start of c*
+  int64_t ttl_base;
+};
+
+struct KeyCtx {
+  int64_t Te, tau;
+  uint32_t smax;
+  int64_t den, num;
+  int64_t ttl_max;
+  float alpha, beta, gamma;
+};
+
+// eq:eviction / eq:recency / eq:size in fp32 with explicit round-to-nearest ops (no contraction)
+__device__ __forceinline__ float wa_lru_score(const KeyCtx& x, int64_t t_last, uint32_t size, float P) {
+  int64_t d = x.Te - t_last;
+  float R = x.tau > 0 ? fminf(1.0f, __fdiv_rn(__ll2float_rn(d), __ll2float_rn(x.tau))) : 0.0f;
+  float S = __fdiv_rn(__ll2float_rn((long long)size), __ll2float_rn((long long)x.smax));
+  float a = __fmul_rn(x.alpha, R);
+  float b = __fmul_rn(x.beta, __fsub_rn(1.0f, P));
+  float c = __fmul_rn(x.gamma, S);
+  return __fadd_rn(__fadd_rn(a, b), c);
+}
+
+__device__ __forceinline__ uint32_t quantize_q20(float s) {
+  float f = floorf(__fmul_rn(s, 1048576.0f));
+  if (!(f > 0.0f)) return 0u;  // also maps NaN to 0
+  if (f > 1048576.0f) return 1048576u;
+  return (uint32_t)f;
+}
+
+// Alg. alg:ttl + eq:pressure as exact integers: el < min(ttl * (1 - m/2), TTL_max),
+// m = clamp((occ/C - low) / (high - low), 0, 1) = num / den.
+__device__ __forceinline__ bool ttl_protected(const KeyCtx& x, const OwnerKeyIn& o) {
+  if (o.shared) return o.prot_shared;
+  if (o.fin) return false;
+  int64_t el = x.Te - o.t_call;
+  if (!(el < x.ttl_max)) return false;
+  return 2 * x.den * el < o.ttl_base * (2 * x.den - x.num);
+}
+
+__device__ __forceinline__ uint64_t aeg_key(bool prot, uint32_t q, uint32_t lid) {
+  return ((uint64_t)(!prot) << 63) | ((uint64_t)q << 32) | (uint64_t)lid;
+}
+
+// ------------------------------------------------------------------------------------------
+// host launch helpers (defined in the .cu files)
+// ------------------------------------------------------------------------------------------
+// exclusive scan of n values into out[0..n] (out[n] = total); scratch handled internally
+cudaError_t scan_u64(saga_trace* t, const uint64_t* in, uint64_t* out, uint64_t n);
+cudaError_t scan_u32(saga_trace* t, const uint32_t* in, uint32_t* out, uint64_t n);
+
+saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d);
+saga_status run_placement(saga_trace* t);
+saga_status run_expand(saga_trace* t, uint32_t w);
+saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* next_use_out, uint32_t* lid_out, cudaStream_t s);
+saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga_replay_cfg* cfg, float* score,
+                      uint64_t* key, cudaStream_t s);
+saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint32_t* k, uint32_t n_seg,
+                       const uint64_t* out_off, uint32_t* victim, cudaStream_t s);
+saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
+                       const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s);
+
+// radix sort of (key u32, value = position) pairs: sorted keys and values into *_out
+cudaError_t onesweep_sort_pairs(saga_trace* t, const uint32_t* keys_in, uint64_t n, uint32_t key_bits,
+                                uint32_t* keys_out, uint32_t* vals_out, cudaStream_t s);
+
+}  // namespace saga
+
+#define SAGA_CK(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t _e = (call);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      saga::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__, __LINE__, \
+                      cudaGetErrorString(_e));                                                 \
+      return SAGA_ERR_CUDA;                                                                    \
+    }                                                                                          \
+  } while (0)
+
+#define SAGA_CK_LAUNCH() SAGA_CK(cudaGetLastError())
