@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the SAGA hot path on B200 (BASELINE.json metric: trace accesses/sec of the whole
+AEG score + evict + replay and Belady pipeline; achieved HBM GB/s of the dominant kernel).
+
+One step = one pass of every §8(a) row over one synthetic trace: saga_load_trace (A1 validate,
+A2 placement, A3 streams) -> saga_belady_next_use per owned node (A4) -> W_lo/W_hi all-reduce
+(A8) -> capacity sweep -> saga_replay AEG + BELADY x caps x nodes (A5-A7) -> counter all-reduce
+(A8).  value = access-replays (sum over policies x caps x nodes of the node's stream length)
+per second, max over ranks, inputs resident in HBM; e2e = the same through the public API from
+pinned host buffers with the H2D copy of the trace and the D2H read of the counters timed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace accesses/sec (AEG score+evict+replay, Bélády); HBM GB/s vs B200 peak"
+UNIT = "access-replays/s"
+PROF_NAMES = ["load", "place", "expand", "sort", "segscan", "epoch_stats", "replay", "score", "select"]
+WORKLOADS = {
+    "C1": "tiny trace: 8 sessions x 10 calls, 1 node, 64 KV blocks",
+    "C2": "SWE-bench-shaped: 2000 sessions, 10-100 calls/task, 16-token blocks, 8 nodes, 8+1 caps",
+    "C3": "WebArena-shaped: 5000 sessions, branching AEG, 16 nodes, 8+1 caps",
+    "C4": "64-GPU cluster: 20k sessions, affinity + work stealing, 16 nodes, 32 caps",
+    "C5": "multi-tenant: 100k sessions, 32 nodes, 32 caps",
+}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.dev), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def sweep_for(name):
+    from gen import N_SWEEP, PHYSICAL_CAP, sweep_caps
+    base = name.split("_")[0]
+    return lambda lo, hi: sweep_caps(lo, hi, N_SWEEP.get(base, 8), PHYSICAL_CAP.get(base))
+
+
+def algorithmic_bytes(cat, n_access, n_replay_access, n_calls, key_bits):
+    """Algorithmic HBM bytes per step of each kernel family (DESIGN.md §7 "Roofline")."""
+    passes = max(1, (key_bits + 7) // 8)
+    return {
+        "sort": n_access * (4 + 12 + 16 * (passes - 1)),     # histogram read + pass 1 + later passes
+        "segscan": n_access * 16,                            # sorted (key, pos) read + next_use/lid writes
+        "epoch_stats": n_access * 8,                          # next_use + lid read in stream order
+        "replay": n_replay_access * 8,                        # per access-replay: lid|flags + next_use
+        "expand": n_access * 4,                               # stream write
+        "place": n_calls * 40,
+        "load": n_calls * 40,
+    }.get(cat, 0)
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (oracle/), as it stands, on a bounded sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from gen import make, place_cfg_for
+    from oracle import oracle as O
+    O.build()
+    desc = make(args.config, n_sessions=args.n_sessions)
+    pc = place_cfg_for(desc)
+    nthreads = os.cpu_count() or 1
+    times, reps = [], 0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        o = O.Oracle(desc, pc)
+        lo, hi = 0, 0
+        for w in range(desc.n_nodes):
+            a, b = o.sweep_range(w) if w == 0 else (0, 0)
+            lo, hi = max(lo, a), max(hi, b)
+        caps = sweep_for(args.config)(lo, hi)
+        cap = [caps[len(caps) // 2]]
+        ctr = o.replay_many(3, cap, nodes=[0], nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        reps = int(ctr[:, :, 0, 0].sum())
+        if i >= args.warmup:
+            times.append(dt)
+        del o
+    sec = statistics.median(times)
+    v = reps / sec
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64/fp32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}",
+                       "sample": f"node 0, AEG+BELADY at capacity {cap[0]}, incl. oracle placement/expansion and node-0 next use"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                             "sample": f"{args.config} node 0, 2 policies x 1 capacity ({reps} access-replays/step)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(desc, pc, caps, nthreads):
+    """Oracle timed on a bounded sample: full oracle build (placement, streams) + next use of every
+    node + one replay per (node, policy) at the middle capacity."""
+    from oracle import oracle as O
+    O.build()
+    t0 = time.perf_counter()
+    o = O.Oracle(desc, pc)
+    cap = [caps[len(caps) // 2]]
+    ctr = o.replay_many(3, cap, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    reps = int(ctr[:, :, :, 0].sum())
+    return {"value": reps / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": f"{desc.name}: oracle build + all {desc.n_nodes} nodes x AEG+BELADY at capacity {cap[0]} "
+                      f"({reps} access-replays in {dt:.1f} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--n-sessions", type=int, default=None)
+    ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from gen import make, place_cfg_for
+    from paper_2605_00528_b200 import pipeline, saga
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    desc = make(args.config, n_sessions=args.n_sessions)
+    pc = place_cfg_for(desc)
+    rcfg = dict(policy_mask=3)
+    caps_fn = sweep_for(args.config)
+    shard_caps = desc.n_nodes == 1 and world > 1
+    comm = saga.Comm(rank, world, local) if world > 1 else None
+    stream = torch.cuda.Stream(device=dev)
+    host_pinned = saga.HostDesc(desc, pinned=True)
+    # device-resident descriptor for `value` (the library deep-copies it device-to-device)
+    dev_keep = []
+    dptrs = []
+    for name, dt in saga.DESC_ARRAYS:
+        a = np.ascontiguousarray(getattr(desc, name), dtype=dt)
+        t = torch.from_numpy(a.view(np.uint8).copy() if a.size else np.zeros(1, np.uint8)).to(dev)
+        dev_keep.append(t)
+        dptrs.append(t.data_ptr())
+
+    class DevDesc:
+        pass
+    dd = DevDesc()
+    dd.keep = dev_keep
+    dd.c = saga.TraceDescC(desc.n_calls, desc.n_sessions, desc.n_types, desc.n_aeg_nodes, desc.n_edges, desc.n_ranges,
+                           desc.n_blocks, desc.n_nodes, desc.block_tokens, *dptrs)
+    counters = None
+
+    def step(host):
+        nonlocal counters
+        with torch.cuda.stream(stream):
+            t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=rank, world=world, comm=comm, device=local,
+                                             stream=stream, host=host, counters=counters, shard_caps=shard_caps)
+        counters = ctr
+        return t, caps, ctr
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # ---- warm-up ----
+    for _ in range(args.warmup):
+        t, caps, _ = step(dd)
+        t.free()
+    torch.cuda.synchronize()
+    # per-step work (access-replays over all ranks)
+    t, caps, ctr = step(dd)
+    stream.synchronize()
+    mine = pipeline.owned_nodes(desc.n_nodes, rank, world) if not shard_caps else [0]
+    n_acc_local = sum(t.info(w)[0] for w in mine)
+    n_pol = 2
+    if shard_caps:
+        n_caps_local = len([i for i in range(len(caps)) if i % world == rank])
+        rep_local = n_acc_local * n_pol * n_caps_local
+    else:
+        rep_local = n_acc_local * n_pol * len(caps)
+    t.free()
+    tot = torch.tensor([rep_local, n_acc_local if not shard_caps or rank == 0 else 0], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    replay_accesses, n_access = int(tot[0]), int(tot[1])
+
+    # ---- timed region (device-resident inputs) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    saga.lib.saga_profile_enable(1)
+    saga.lib.saga_profile_read(None, None)
+    l0 = saga.kernel_launches()
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        t, caps, ctr = step(dd)
+        t.free()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = saga.kernel_launches() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    import ctypes as C
+    pm = (C.c_double * 9)()
+    pn = (C.c_uint64 * 9)()
+    saga.lib.saga_profile_read(pm, pn)
+    saga.lib.saga_profile_enable(0)
+    clocks = sampler.stop()
+    mt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+    ms = float(mt[0])
+    value = replay_accesses / (ms / 1e3)
+    counters_host = ctr.cpu().numpy()
+
+    # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out_host = torch.empty(tuple(ctr.shape), dtype=torch.int64, pin_memory=True)
+        for _ in range(args.steps):
+            t, caps, c2 = step(host_pinned)
+            with torch.cuda.stream(stream):
+                out_host.copy_(c2, non_blocking=True)
+            stream.synchronize()
+            t.free()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = e0.elapsed_time(e1) / args.steps
+        et = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        ems = float(et[0])
+        e2e = {"value": replay_accesses / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": host_pinned.nbytes,
+               "d2h_bytes_per_step": int(out_host.numel() * 8), "ms_per_step": ems}
+        assert np.array_equal(out_host.numpy(), counters_host), "e2e counters differ from the device-resident run"
+
+    # ---- roofline of the dominant kernel family (per-launch, CUDA events on the launching stream) ----
+    peak, peak_kind = hbm_peak()
+    key_bits = int(np.ceil(np.log2(max(desc.n_blocks, 2))))
+    kernels = {}
+    for i, nm in enumerate(PROF_NAMES):
+        if pn[i] == 0:
+            continue
+        ms_k = pm[i] / args.steps
+        byt = algorithmic_bytes(nm, n_access / max(world, 1) if not shard_caps else n_access,
+                                replay_accesses / max(world, 1), desc.n_calls, key_bits)
+        kernels[nm] = {"ms_per_step": ms_k, "launches_per_step": pn[i] / args.steps, "share": ms_k / ms,
+                       "algorithmic_gb_s": (byt / (ms_k / 1e3) / 1e9) if byt and ms_k > 0 else None}
+    dom = max((k for k in kernels if k in ("sort", "segscan", "epoch_stats", "replay", "expand")),
+              key=lambda k: kernels[k]["ms_per_step"], default=None)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if dom and os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(dom)
+        except Exception:
+            traffic = None
+    roof = None
+    if dom:
+        ach = kernels[dom]["algorithmic_gb_s"] or 0.0
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "peak_source": peak_kind,
+                "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(desc, pc, caps, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64/fp32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "trace": desc.name,
+                       "nodes": desc.n_nodes, "caps": caps, "policies": ["AEG", "BELADY"],
+                       "trace_accesses": n_access, "access_replays_per_step": replay_accesses,
+                       "trace_accesses_per_s": n_access / (ms / 1e3),
+                       "l2": "inputs larger than L2 (node streams 4 B/access + per-node next-use arrays)",
+                       "sharding": "capacity points" if shard_caps else "cache nodes w mod R"},
+            "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels,
+            "counters_checksum": int(np.bitwise_xor.reduce(counters_host.reshape(-1).view(np.uint64))),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -241,6 +241,24 @@ void saga_comm_destroy(saga_comm* c);
 /* Number of libsaga kernels launched by this process so far (for bench.py's gpu_launches). */
 uint64_t saga_kernel_launches(void);
 
+/* Optional device-time profile (CUDA events recorded on the launching stream around each kernel
+ * family).  saga_profile_read syncs, writes the accumulated milliseconds and launch counts of
+ * every category into ms_out[SAGA_PROF_NCAT] / n_out[SAGA_PROF_NCAT] (nullable), and resets. */
+enum {
+  SAGA_PROF_LOAD = 0,      /* A1 validate + derive (includes the H2D copy of the descriptor)   */
+  SAGA_PROF_PLACE = 1,     /* A2 placement kernel                                             */
+  SAGA_PROF_EXPAND = 2,    /* A3 stream expansion (span of its launches)                      */
+  SAGA_PROF_SORT = 3,      /* A4 histogram + onesweep passes                                  */
+  SAGA_PROF_SEGSCAN = 4,   /* A4 segmented scans -> next_use / local ids                      */
+  SAGA_PROF_EPOCH = 5,     /* A4 per-epoch statistics (first-in-epoch, W_lo / W_hi)          */
+  SAGA_PROF_REPLAY = 6,    /* A5-A7 replay kernel                                             */
+  SAGA_PROF_SCORE = 7,     /* A5 bulk score                                                   */
+  SAGA_PROF_SELECT = 8,    /* A6 bulk select                                                  */
+  SAGA_PROF_NCAT = 9
+};
+void saga_profile_enable(int on);
+void saga_profile_read(double* ms_out, uint64_t* n_out);
+
 void saga_free_trace(saga_trace* t);
 
 #ifdef __cplusplus

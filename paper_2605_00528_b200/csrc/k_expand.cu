@@ -142,6 +142,7 @@ __global__ void k_fill_stream(TraceView v, const uint32_t* g_call, const uint64_
 }  // namespace
 
 saga_status run_expand(saga_trace* t, uint32_t w) {
+  ProfScope prof(SAGA_PROF_EXPAND, t->stream);
   const TraceView& v = t->v;
   NodeDev& nd = t->nodes[w];
   cudaStream_t s = t->stream;

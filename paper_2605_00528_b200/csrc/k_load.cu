@@ -178,7 +178,7 @@ saga_status upload(saga_trace* t, const T* src, size_t n, const T** dst, bool re
   }
   T* p = dalloc<T>(t, n);
   if (!p) { set_error("saga_load_trace: out of device memory"); return SAGA_ERR_OOM; }
-  SAGA_CK(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, t->stream));
+  SAGA_CK(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyDefault, t->stream));  // host or device (UVA)
   *dst = p;
   return SAGA_OK;
 }
@@ -186,6 +186,7 @@ saga_status upload(saga_trace* t, const T* src, size_t n, const T** dst, bool re
 }  // namespace
 
 saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d) {
+  ProfScope prof(SAGA_PROF_LOAD, t->stream);
   TraceView& v = t->v;
   v.n_calls = d->n_calls; v.n_sessions = d->n_sessions; v.n_types = d->n_types; v.n_aeg = d->n_aeg_nodes;
   v.n_edges = d->n_edges; v.n_ranges = d->n_ranges; v.n_blocks = d->n_blocks; v.n_nodes = d->n_nodes;

@@ -249,7 +249,9 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     SAGA_CK(onesweep_sort_pairs(t, nd.block, N, key_bits, skey, sval, s));
     // K5: segmented scans in sorted order
     if (N > 0) {
+      prof_begin(SAGA_PROF_SEGSCAN, s);
       k_segscan<<<(unsigned)tiles, SS_T, 0, s>>>(skey, sval, N, v.owner, nd.nxt, nd.lidf, lown, status, tctr, nl);
+      prof_end(SAGA_PROF_SEGSCAN, s);
       count_launch();
     }
     // per-event statistics in stream order
@@ -262,6 +264,7 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     cl = cf + J;
     sw = cl + J;
     SAGA_CK(cudaMemsetAsync(cd, 0, size_t(J) * 12 + 16, s));
+    prof_begin(SAGA_PROF_EPOCH, s);
     k_ev_pos<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(nd.g_pos, nd.ev_g, J, ev_pos);
     count_launch();
     if (N > 0) {
@@ -269,6 +272,7 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
       count_launch();
     }
     k_sweep<<<1, SS_T, 0, s>>>(cd, cf, cl, Jr, sw);
+    prof_end(SAGA_PROF_EPOCH, s);
     count_launch();
     uint32_t hw[2] = {0, 0}, hn = 0;
     SAGA_CK(cudaMemcpyAsync(hw, sw, 8, cudaMemcpyDeviceToHost, s));

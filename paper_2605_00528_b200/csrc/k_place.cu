@@ -343,7 +343,9 @@ saga_status run_placement(saga_trace* t) {
   a.node_of = t->node_of; a.migs = t->migs; a.mig_cap = mig_cap; a.act = t->act; a.act_cap = act_cap;
   a.out_n = out_n; a.out_stats = out_stats; a.aff = aff; a.last_c = lastc; a.moved = moved; a.fin = fin;
   SAGA_CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  prof_begin(SAGA_PROF_PLACE, t->stream);
   k_place<<<1, 32, smem, t->stream>>>(a);
+  prof_end(SAGA_PROF_PLACE, t->stream);
   count_launch();
   SAGA_CK_LAUNCH();
   uint32_t hn[4];

@@ -458,7 +458,9 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   a.slot_of = slot_of; a.sl_lid = sl_lid; a.sl_t = sl_t; a.sl_nu = sl_nu; a.sl_own = sl_own; a.sl_stamp = sl_stamp;
   a.kbuf = kbuf; a.kslot = kslot; a.sstate = sstate; a.max_local = max_local; a.slot_cap = slot_cap;
   a.work = work; a.err = err;
+  prof_begin(SAGA_PROF_REPLAY, s);
   k_replay<<<grid, RT, 0, s>>>(a);
+  prof_end(SAGA_PROF_REPLAY, s);
   count_launch();
   SAGA_CK_LAUNCH();
   uint32_t herr = 0;

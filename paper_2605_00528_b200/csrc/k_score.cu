@@ -200,7 +200,9 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
   a.p_low = cfg->p_low_pm; a.p_high = cfg->p_high_pm; a.ttl_max = cfg->ttl_max_us;
   a.score = score; a.key = key;
   const unsigned grid = std::min<unsigned>(b->n_seg, nsm_count());
+  prof_begin(SAGA_PROF_SCORE, s);
   k_score<<<grid, ST, 0, s>>>(a);
+  prof_end(SAGA_PROF_SCORE, s);
   count_launch();
   SAGA_CK_LAUNCH();
   cudaFreeAsync(dn, s);
@@ -223,7 +225,9 @@ saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint3
   uint32_t* si = nullptr;
   SAGA_CK(cudaMallocAsync((void**)&sk, 8 * np2 * grid, s));
   SAGA_CK(cudaMallocAsync((void**)&si, 4 * np2 * grid, s));
+  prof_begin(SAGA_PROF_SELECT, s);
   k_select<<<grid, SLT, 0, s>>>(key, seg_off, k, n_seg, out_off, victim, sk, si, np2);
+  prof_end(SAGA_PROF_SELECT, s);
   count_launch();
   SAGA_CK_LAUNCH();
   cudaFreeAsync(sk, s);

@@ -209,6 +209,7 @@ cudaError_t onesweep_sort_pairs(saga_trace* t, const uint32_t* keys_in, uint64_t
                                 uint32_t* vals_out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   if (key_bits < 1) key_bits = 1;
+  ProfScope prof(SAGA_PROF_SORT, s);
   const int npass = (int)((key_bits + RBITS - 1) / RBITS);
   const uint64_t tiles = (n + TILE - 1) / TILE;
   uint32_t *kA = nullptr, *vA = nullptr, *hist = nullptr, *status = nullptr, *tctr = nullptr;

@@ -19,6 +19,45 @@ void set_error(const char* fmt, ...) {
   g_err = buf;
 }
 
+// ---------------- profile: CUDA event pairs per kernel family ----------------
+namespace prof_detail {
+struct ProfRec { int cat; cudaEvent_t a, b; };
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_pool;
+thread_local std::vector<std::pair<int, cudaEvent_t>> g_prof_open;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) { cudaEvent_t e = g_prof_pool.back(); g_prof_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace prof_detail
+using namespace prof_detail;
+
+void prof_begin(int cat, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, s);
+  g_prof_open.push_back({cat, e});
+}
+
+void prof_end(int cat, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  for (size_t i = g_prof_open.size(); i-- > 0;) {
+    if (g_prof_open[i].first != cat) continue;
+    cudaEvent_t b = prof_event();
+    cudaEventRecord(b, s);
+    g_prof.push_back({cat, g_prof_open[i].second, b});
+    g_prof_open.erase(g_prof_open.begin() + (long)i);
+    return;
+  }
+}
+
 static void mempool_setup(int device) {
   static std::mutex mu;
   static uint64_t done_mask = 0;
@@ -54,6 +93,32 @@ extern "C" {
 const char* saga_last_error(void) { return g_err.c_str(); }
 
 uint64_t saga_kernel_launches(void) { return g_launches.load(); }
+
+void saga_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+void saga_profile_read(double* ms_out, uint64_t* n_out) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  double ms[SAGA_PROF_NCAT] = {0};
+  uint64_t n[SAGA_PROF_NCAT] = {0};
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float x = 0.f;
+    if (cudaEventElapsedTime(&x, r.a, r.b) == cudaSuccess && r.cat >= 0 && r.cat < SAGA_PROF_NCAT) {
+      ms[r.cat] += x;
+      n[r.cat] += 1;
+    }
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  for (int i = 0; i < SAGA_PROF_NCAT; ++i) {
+    if (ms_out) ms_out[i] = ms[i];
+    if (n_out) n_out[i] = n[i];
+  }
+}
 
 void saga_free_trace(saga_trace* t) {
   if (!t) return;

@@ -26,6 +26,16 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 void set_error(const char* fmt, ...);
 
+// device-time profile (saga_profile_enable / saga_profile_read)
+void prof_begin(int cat, cudaStream_t s);
+void prof_end(int cat, cudaStream_t s);
+struct ProfScope {
+  int cat;
+  cudaStream_t s;
+  ProfScope(int c, cudaStream_t st) : cat(c), s(st) { prof_begin(cat, s); }
+  ~ProfScope() { prof_end(cat, s); }
+};
+
 struct Mig { uint32_t e, s, v, t; };
 struct ActRec { uint32_t e, w, mask, pad; };
 

@@ -84,6 +84,8 @@ def _load():
         "saga_allreduce_counters": (i32, [vp, vp, C.c_size_t, i32, vp]),
         "saga_comm_destroy": (None, [vp]),
         "saga_free_trace": (None, [vp]),
+        "saga_profile_enable": (None, [i32]),
+        "saga_profile_read": (None, [vp, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
