@@ -32,7 +32,8 @@ __device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned lon
 __global__ void __launch_bounds__(SS_T) k_segscan(const uint32_t* __restrict__ skey, const uint32_t* __restrict__ sval,
                                                   uint64_t n, const uint32_t* __restrict__ owner,
                                                   uint32_t* __restrict__ nxt, uint32_t* __restrict__ lidf,
-                                                  uint32_t* __restrict__ lown, unsigned long long* status,
+                                                  uint32_t* __restrict__ lown, uint32_t* __restrict__ l2g,
+                                                  unsigned long long* status,
                                                   uint32_t* tile_counter, uint32_t* n_local_out) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t wsum[SS_T / 32];
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(SS_T) k_segscan(const uint32_t* __restrict__ s
     else nv = has_next ? sval[j + 1] : 0u;
     nxt[pos] = has_next ? nv : INF32;
     lidf[pos] = l | (head ? LID_FTN : 0u);
-    if (head) lown[l] = owner[k[i]];
+    if (head) { lown[l] = owner[k[i]]; l2g[l] = k[i]; }
     if (j == n - 1) *n_local_out = l + 1;
   }
 }
@@ -233,12 +234,13 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
       if (!nd.lidf || !nd.nxt) { set_error("out of device memory (next use)"); return SAGA_ERR_OOM; }
     }
     uint32_t key_bits = 32 - __builtin_clz(v.n_blocks > 1 ? v.n_blocks - 1 : 1);
-    uint32_t *skey = nullptr, *sval = nullptr, *lown = nullptr, *tctr = nullptr, *nl = nullptr;
+    uint32_t *skey = nullptr, *sval = nullptr, *lown = nullptr, *l2g = nullptr, *tctr = nullptr, *nl = nullptr;
     unsigned long long* status = nullptr;
     const uint64_t tiles = (N + SS_TILE - 1) / SS_TILE;
     SAGA_CK(cudaMallocAsync((void**)&skey, std::max<uint64_t>(N, 1) * 4, s));
     SAGA_CK(cudaMallocAsync((void**)&sval, std::max<uint64_t>(N, 1) * 4, s));
     SAGA_CK(cudaMallocAsync((void**)&lown, std::max<uint64_t>(N, 1) * 4, s));
+    SAGA_CK(cudaMallocAsync((void**)&l2g, std::max<uint64_t>(N, 1) * 4, s));
     SAGA_CK(cudaMallocAsync((void**)&status, std::max<uint64_t>(tiles, 1) * 8, s));
     SAGA_CK(cudaMallocAsync((void**)&tctr, 8, s));
     SAGA_CK(cudaMallocAsync((void**)&nl, 4, s));
@@ -250,7 +252,8 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     // K5: segmented scans in sorted order
     if (N > 0) {
       prof_begin(SAGA_PROF_SEGSCAN, s);
-      k_segscan<<<(unsigned)tiles, SS_T, 0, s>>>(skey, sval, N, v.owner, nd.nxt, nd.lidf, lown, status, tctr, nl);
+      k_segscan<<<(unsigned)tiles, SS_T, 0, s>>>(skey, sval, N, v.owner, nd.nxt, nd.lidf, lown, l2g, status, tctr,
+                                                        nl);
       prof_end(SAGA_PROF_SEGSCAN, s);
       count_launch();
     }
@@ -283,8 +286,10 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     nd.w_hi = hw[1];
     nd.n_local = hn;
     nd.lown = dalloc<uint32_t>(t, hn);
-    if (!nd.lown) { set_error("out of device memory (next use)"); return SAGA_ERR_OOM; }
+    nd.lid2gid = dalloc<uint32_t>(t, hn);
+    if (!nd.lown || !nd.lid2gid) { set_error("out of device memory (next use)"); return SAGA_ERR_OOM; }
     SAGA_CK(cudaMemcpyAsync(nd.lown, lown, size_t(hn) * 4, cudaMemcpyDeviceToDevice, s));
+    SAGA_CK(cudaMemcpyAsync(nd.lid2gid, l2g, size_t(hn) * 4, cudaMemcpyDeviceToDevice, s));
     // update list: calls of the sessions that own a block at this node (replay session state)
     const uint32_t nc = v.n_calls;
     uint32_t *present = nullptr, *flag = nullptr, *pos = nullptr;
@@ -308,6 +313,7 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     cudaFreeAsync(skey, s);
     cudaFreeAsync(sval, s);
     cudaFreeAsync(lown, s);
+    cudaFreeAsync(l2g, s);
     cudaFreeAsync(status, s);
     cudaFreeAsync(tctr, s);
     cudaFreeAsync(nl, s);

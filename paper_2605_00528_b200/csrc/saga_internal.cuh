@@ -104,8 +104,20 @@ struct NodeDev {
   uint32_t* lidf = nullptr;    // [N] local id | LID_FTN | LID_NFIE
   uint32_t* nxt = nullptr;     // [N] next use
   uint32_t* lown = nullptr;    // [n_local] owner of the local block
+  uint32_t* lid2gid = nullptr; // [n_local] global block id of the local block (ascending)
   uint32_t n_upd = 0;
   uint32_t* upd_c = nullptr;   // calls of sessions present at the node (call order)
+  // replay index (built once per node by the first saga_replay, DESIGN.md §6 "replay state")
+  bool rp_done = false;
+  uint32_t n_units = 0;        // maximal runs of positions with the same (record group, owner)
+  uint32_t max_ev_units = 0;   // most units in one event
+  uint64_t* ev_pos = nullptr;  // [J+1] first position of event j
+  uint32_t* ev_unit = nullptr; // [J+1] first unit of event j
+  uint32_t* ev_upd = nullptr;  // [J] end of the session-update list for event j
+  uint32_t* u_of = nullptr;    // [N] unit of position p | KIND_MIG
+  uint32_t* u_pos = nullptr;   // [n_units+1] first position of unit u
+  int64_t* u_t = nullptr;      // [n_units] t of the unit's record group (t_c or T_e for MIG)
+  uint32_t* u_own = nullptr;   // [n_units] owner of the unit's blocks
 };
 
 }  // namespace saga

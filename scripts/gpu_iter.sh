@@ -1,0 +1,11 @@
+#!/bin/bash
+# quick iteration on one B200: build, GPU parity tests, one C2 bench line (no oracle timing)
+cd ${GRAFT_REPO_ROOT:-.}
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+timeout ${TEST_TIMEOUT:-900} python -m pytest tests -m gpu -x -q -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/gpu_tests.log 2>&1; echo "pytest exit $?" >> gpurun_out/gpu_tests.log
+tail -15 gpurun_out/gpu_tests.log
+if [ -n "${BENCH_ARGS+x}" ]; then
+  timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
+  tail -c 2500 gpurun_out/bench.log
+fi
