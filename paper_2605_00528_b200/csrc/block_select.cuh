@@ -1,5 +1,11 @@
-// Block-level building blocks shared by the replay (A7) and the bulk select (A6) kernels:
-// reductions, an exclusive scan, and radix select of the k largest unique uint64 keys.
+// Block-level building blocks shared by the replay (A7) and the bulk score/select (A5/A6)
+// kernels: reductions, an exclusive scan, and radix select of the k largest unique uint64 keys.
+//
+// Every collective costs ONE __syncthreads: warp partials go to a double-buffered slot in shared
+// memory and every warp finishes the combine with shuffles.  A thread can only overwrite a slot
+// two collectives later, after the barrier of the collective in between, which every thread
+// reaches only once it has read the slot -- so no second barrier is needed.  `Par` carries the
+// slot parity; all threads execute the same sequence of collectives, so their parities agree.
 #pragma once
 #include "saga_internal.cuh"
 
@@ -10,58 +16,69 @@ struct Max { template <class T> __device__ T operator()(T a, T b) const { return
 struct Or { template <class T> __device__ T operator()(T a, T b) const { return a | b; } };
 struct And { template <class T> __device__ T operator()(T a, T b) const { return a & b; } };
 
+struct Par { uint32_t p = 0; };
+
 template <int BT>
 struct BlockScratch {
-  uint32_t u32[BT / 32];
-  unsigned long long u64[BT / 32];
-  long long i64[BT / 32];
+  static constexpr int NW = BT / 32;
+  static_assert((NW & (NW - 1)) == 0 && NW <= 32, "block size must be 32 x power of two");
+  unsigned long long part[2][NW];
   uint32_t hist[256];
   uint32_t sel_d, sel_above;
 };
 
 template <int BT, class T, class Op>
-__device__ __forceinline__ T block_reduce(T x, Op op, T* scratch /*[BT/32]*/) {
+__device__ __forceinline__ T block_reduce(T x, Op op, BlockScratch<BT>& sm, Par& par) {
+  constexpr int NW = BT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(0xffffffffu, x, o));
-  if (lane == 0) scratch[wid] = x;
+  T* buf = reinterpret_cast<T*>(sm.part[par.p]);
+  par.p ^= 1u;
+  if (lane == 0) buf[wid] = x;
   __syncthreads();
-  T r = scratch[0];
+  T y = buf[lane & (NW - 1)];
 #pragma unroll
-  for (int w = 1; w < BT / 32; ++w) r = op(r, scratch[w]);
-  __syncthreads();
-  return r;
+  for (int o = NW / 2; o > 0; o >>= 1) y = op(y, __shfl_xor_sync(0xffffffffu, y, o));
+  return y;
 }
 
 // exclusive scan of one value per thread; *total receives the block sum
 template <int BT>
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* scratch /*[BT/32]*/) {
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, BlockScratch<BT>& sm, Par& par) {
+  constexpr int NW = BT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) scratch[wid] = x;
+  uint32_t* buf = reinterpret_cast<uint32_t*>(sm.part[par.p]);
+  par.p ^= 1u;
+  if (lane == 31) buf[wid] = x;
   __syncthreads();
-  uint32_t pre = 0, tot = 0;
+  const uint32_t y0 = buf[lane & (NW - 1)];
+  uint32_t y = y0;
 #pragma unroll
-  for (int w = 0; w < BT / 32; ++w) { uint32_t s = scratch[w]; if (w < wid) pre += s; tot += s; }
-  __syncthreads();
-  *total = tot;
-  return pre + x - v;
+  for (int o = 1; o < NW; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, y, o, NW);
+    if ((lane & (NW - 1)) >= o) y += t;
+  }
+  *total = __shfl_sync(0xffffffffu, y, NW - 1);
+  return __shfl_sync(0xffffffffu, y - y0, wid) + x - v;
 }
 
-// Threshold T with #{i : kb[i] >= T} == k for n unique keys and 1 <= k <= n.
-// Radix select from the highest bit on which the keys differ, 8-bit digits, early exit when the
-// pivot bucket is consumed exactly.  Every pass re-reads kb (L2-resident for replay sizes).
+// Threshold T with #{i : kb[i] >= T} == k for n keys, 1 <= k <= n, where the keys are unique
+// except possibly for copies of the value 0 and T > 0 (the replay pads with zeros).  Radix select
+// from the highest bit on which the keys differ, 8-bit digits, early exit when the pivot bucket
+// is consumed exactly.  Every pass re-reads kb (L2-resident for replay sizes).
 template <int BT>
-__device__ uint64_t radix_select(const uint64_t* kb, uint32_t n, uint32_t k, BlockScratch<BT>& sm) {
+__device__ uint64_t radix_select(const uint64_t* kb, uint32_t n, uint32_t k, BlockScratch<BT>& sm, Par& par) {
   unsigned long long o = 0, an = ~0ull;
   for (uint32_t i = threadIdx.x; i < n; i += BT) { const uint64_t x = kb[i]; o |= x; an &= x; }
-  o = block_reduce<BT, unsigned long long>(o, Or(), sm.u64);
-  an = block_reduce<BT, unsigned long long>(an, And(), sm.u64);
+  o = block_reduce<BT, unsigned long long>(o, Or(), sm, par);
+  an = block_reduce<BT, unsigned long long>(an, And(), sm, par);
   const unsigned long long diff = o ^ an;
   if (diff == 0) return o;
   const int top = 63 - __clzll(diff);

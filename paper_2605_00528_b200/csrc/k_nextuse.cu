@@ -237,13 +237,13 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     uint32_t *skey = nullptr, *sval = nullptr, *lown = nullptr, *l2g = nullptr, *tctr = nullptr, *nl = nullptr;
     unsigned long long* status = nullptr;
     const uint64_t tiles = (N + SS_TILE - 1) / SS_TILE;
-    SAGA_CK(cudaMallocAsync((void**)&skey, std::max<uint64_t>(N, 1) * 4, s));
-    SAGA_CK(cudaMallocAsync((void**)&sval, std::max<uint64_t>(N, 1) * 4, s));
-    SAGA_CK(cudaMallocAsync((void**)&lown, std::max<uint64_t>(N, 1) * 4, s));
-    SAGA_CK(cudaMallocAsync((void**)&l2g, std::max<uint64_t>(N, 1) * 4, s));
-    SAGA_CK(cudaMallocAsync((void**)&status, std::max<uint64_t>(tiles, 1) * 8, s));
-    SAGA_CK(cudaMallocAsync((void**)&tctr, 8, s));
-    SAGA_CK(cudaMallocAsync((void**)&nl, 4, s));
+    SAGA_CK(ws_malloc((void**)&skey, std::max<uint64_t>(N, 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&sval, std::max<uint64_t>(N, 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&lown, std::max<uint64_t>(N, 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&l2g, std::max<uint64_t>(N, 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&status, std::max<uint64_t>(tiles, 1) * 8, s));
+    SAGA_CK(ws_malloc((void**)&tctr, 8, s));
+    SAGA_CK(ws_malloc((void**)&nl, 4, s));
     SAGA_CK(cudaMemsetAsync(status, 0, std::max<uint64_t>(tiles, 1) * 8, s));
     SAGA_CK(cudaMemsetAsync(tctr, 0, 8, s));
     SAGA_CK(cudaMemsetAsync(nl, 0, 4, s));
@@ -261,8 +261,8 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     const uint32_t J = nd.J, Jr = nd.J - 1;
     uint64_t* ev_pos = nullptr;
     uint32_t *cd = nullptr, *cf = nullptr, *cl = nullptr, *sw = nullptr;
-    SAGA_CK(cudaMallocAsync((void**)&ev_pos, (size_t(J) + 1) * 8, s));
-    SAGA_CK(cudaMallocAsync((void**)&cd, size_t(J) * 12 + 16, s));
+    SAGA_CK(ws_malloc((void**)&ev_pos, (size_t(J) + 1) * 8, s));
+    SAGA_CK(ws_malloc((void**)&cd, size_t(J) * 12 + 16, s));
     cf = cd + J;
     cl = cf + J;
     sw = cl + J;
@@ -293,9 +293,9 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     // update list: calls of the sessions that own a block at this node (replay session state)
     const uint32_t nc = v.n_calls;
     uint32_t *present = nullptr, *flag = nullptr, *pos = nullptr;
-    SAGA_CK(cudaMallocAsync((void**)&present, (size_t(v.n_sessions) / 32 + 1) * 4, s));
-    SAGA_CK(cudaMallocAsync((void**)&flag, (size_t(nc) + 1) * 4, s));
-    SAGA_CK(cudaMallocAsync((void**)&pos, (size_t(nc) + 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&present, (size_t(v.n_sessions) / 32 + 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&flag, (size_t(nc) + 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&pos, (size_t(nc) + 1) * 4, s));
     SAGA_CK(cudaMemsetAsync(present, 0, (size_t(v.n_sessions) / 32 + 1) * 4, s));
     k_present<<<grid_for(hn), NTHREADS, 0, s>>>(nd.lown, hn, v.n_sessions, present);
     k_flag_present<<<grid_for(nc), NTHREADS, 0, s>>>(v.call_sess, nc, present, flag);
@@ -310,18 +310,18 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     k_scatter_flag2<<<grid_for(nc), NTHREADS, 0, s>>>(flag, pos, nc, nd.upd_c);
     count_launch();
     SAGA_CK_LAUNCH();
-    cudaFreeAsync(skey, s);
-    cudaFreeAsync(sval, s);
-    cudaFreeAsync(lown, s);
-    cudaFreeAsync(l2g, s);
-    cudaFreeAsync(status, s);
-    cudaFreeAsync(tctr, s);
-    cudaFreeAsync(nl, s);
-    cudaFreeAsync(ev_pos, s);
-    cudaFreeAsync(cd, s);
-    cudaFreeAsync(present, s);
-    cudaFreeAsync(flag, s);
-    cudaFreeAsync(pos, s);
+    ws_free(skey, s);
+    ws_free(sval, s);
+    ws_free(lown, s);
+    ws_free(l2g, s);
+    ws_free(status, s);
+    ws_free(tctr, s);
+    ws_free(nl, s);
+    ws_free(ev_pos, s);
+    ws_free(cd, s);
+    ws_free(present, s);
+    ws_free(flag, s);
+    ws_free(pos, s);
     nd.nu_done = true;
   }
   if ((nu_out || lid_out) && N > 0) {

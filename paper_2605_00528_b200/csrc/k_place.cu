@@ -3,11 +3,16 @@
 // P:766).  Rules P1-P6 of DESIGN.md §4.2.
 //
 // The method is sequential in time (every boundary depends on the previous one), so this is a
-// single warp: lane w owns cache node w (n_nodes <= 32).  Queues live in shared memory
-// (per-node FIFO arrays of (call | started, remaining us)); per-session state in global memory.
-// Epochs in which nothing can happen but service (no admission, every queued call already in
-// service so no victim can exist) are advanced in closed form, so the loop visits only
-// admission epochs and epochs with waiting calls.
+// single warp: lane w owns cache node w (n_nodes <= 32).  Its cost is the latency of one
+// boundary, so the kernel is built around keeping that latency short:
+//   * per-call inputs are packed by a parallel pre-pass into one 32-byte record (session, e(c),
+//     work if routed to a cached affinity / elsewhere, type and flags, ttl, tool start);
+//   * per-session routing state is one 16-byte record (affinity, fin, terminal/ttl/tool start of
+//     the session's last call), held in shared memory when the session table fits;
+//   * the records of the next 32 calls (and their sessions) are loaded while the current boundary
+//     is still being processed, so a boundary normally waits on no global-memory round trip;
+//   * queues are per-node FIFO arrays in shared memory; epochs in which nothing can happen but
+//     service (no admission, every queued call in service) are advanced in closed form.
 #include "saga_internal.cuh"
 
 namespace saga {
@@ -16,9 +21,26 @@ namespace {
 constexpr uint32_t STARTED = 1u << 31;
 constexpr uint32_t CMASK = STARTED - 1;
 constexpr uint64_t PHI = 0x9E3779B97F4A7C15ull;
+constexpr uint32_t F_FNEW = 1u << 16;  // is_last || terminal(v): the session finishes with this call
+constexpr uint32_t F_TERM = 1u << 17;  // terminal(v)
+
+struct __align__(16) CallRec {
+  uint32_t s, e, om_cached, om_full;  // work (us) if routed to its cached affinity / elsewhere
+  uint32_t tyf;                       // session type | F_FNEW | F_TERM
+  uint32_t ttl;                       // ttl_base of the call's AEG node (<= 1e9, validated)
+  int64_t tend;                       // tool start t_c + prefill(new) + decode(out)
+};
+constexpr uint32_t S_FIN = 1u << 30;   // session finished (no affinity count)
+constexpr uint32_t S_TERM = 1u << 31;  // the last call's AEG node is terminal
+struct __align__(16) SessRec {
+  int32_t aff;     // affinity node or -1
+  uint32_t ttlf;   // ttl_base of the last call's node (< 2^30) | S_FIN | S_TERM
+  int64_t tend_lv; // tool start of the last call
+};
 
 struct PlaceArgs {
   TraceView v;
+  const CallRec* rec;
   uint32_t kappa, theta_pm, rmax_pm, qcap;
   int64_t t_idle_us;
   uint64_t seed;
@@ -27,13 +49,28 @@ struct PlaceArgs {
   uint32_t mig_cap;
   ActRec* act;
   uint32_t act_cap;
-  uint32_t* out_n;               // [0] n_mig, [1] n_act, [2] error (1 queue overflow, 2 log overflow)
+  uint32_t* out_n;               // [0] n_mig, [1] n_act, [2] error (1 queue overflow, 2 log overflow, 4 transfer)
   unsigned long long* out_stats; // [0] steals, [1] reroutes
-  volatile int32_t* aff;
-  volatile int32_t* last_c;
-  volatile uint8_t* moved;
-  volatile uint8_t* fin;
+  SessRec* sess_g;               // session table in global memory (when it does not fit in smem)
+  uint8_t* moved_g;
 };
+
+__global__ void k_call_rec(TraceView v, CallRec* rec) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < v.n_calls; c += gridDim.x * blockDim.x) {
+    const uint32_t s = v.call_sess[c], vc = v.call_v[c];
+    const int64_t dec = ceil_div64((int64_t)v.call_out[c] * 1000000, v.decode_tok_s);
+    CallRec r;
+    r.s = s;
+    r.e = v.ecall[c];
+    r.om_cached = (uint32_t)(ceil_div64((int64_t)v.call_new[c] * 1000000, v.prefill_tok_s) + dec);
+    r.om_full = (uint32_t)(ceil_div64((int64_t)v.call_prompt[c] * 1000000, v.prefill_tok_s) + dec);
+    const bool term = v.term[vc] != 0;
+    r.tyf = (uint32_t)v.styp[s] | ((v.call_last[c] || term) ? F_FNEW : 0u) | (term ? F_TERM : 0u);
+    r.ttl = (uint32_t)v.ttl[vc];
+    r.tend = v.tend[c];
+    rec[c] = r;
+  }
+}
 
 __device__ __forceinline__ int64_t warp_min64(int64_t x) {
 #pragma unroll
@@ -41,12 +78,18 @@ __device__ __forceinline__ int64_t warp_min64(int64_t x) {
   return x;
 }
 
+template <bool SS>
 __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t W = a.v.n_nodes, lane = threadIdx.x, K = a.kappa, Q = a.qcap;
   const int64_t E = a.v.epoch_us;
-  uint32_t* qc = smem + lane * Q;                       // call | STARTED
-  uint32_t* qr = smem + W * Q + lane * Q;               // remaining work (us)
+  const TraceView& v = a.v;
+  const uint32_t NS = v.n_sessions, NC = v.n_calls;
+  SessRec* sess = SS ? reinterpret_cast<SessRec*>(smem_raw) : a.sess_g;
+  uint8_t* moved = SS ? smem_raw + (size_t)NS * sizeof(SessRec) : a.moved_g;
+  const size_t qoff = SS ? (((size_t)NS * (sizeof(SessRec) + 1) + 15) & ~(size_t)15) : 0;
+  uint32_t* qc = reinterpret_cast<uint32_t*>(smem_raw + qoff) + lane * Q;          // session | STARTED
+  uint32_t* qr = reinterpret_cast<uint32_t*>(smem_raw + qoff) + W * Q + lane * Q;  // remaining work (us)
   __shared__ int32_t cnt[32][32];                       // sessions with aff = w, !fin, by type
   __shared__ int32_t act_tot[32];
   __shared__ uint32_t xfer_c[64], xfer_r[64];
@@ -54,14 +97,31 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   __shared__ unsigned long long steals, reroutes;
   for (int i = lane; i < 32 * 32; i += 32) (&cnt[0][0])[i] = 0;
   act_tot[lane] = 0;
+  if (SS) {
+    const SessRec init{-1, 0u, 0ll};
+    for (uint32_t i = lane; i < NS; i += 32) { sess[i] = init; moved[i] = 0; }
+  }
   if (lane == 0) { n_mig = 0; n_act = 0; errf = 0; steals = 0; reroutes = 0; xfer_n = 0; }
   __syncwarp();
   const bool act_lane = lane < W;
   uint32_t len = 0;
   int64_t L = 0, idle = 0;
-  const TraceView& v = a.v;
   uint32_t next = 0;
   uint64_t e = 1;
+
+  // prefetched inputs of calls next .. next + 31 (lane i holds call next + i)
+  CallRec pre;
+  SessRec ps;
+  auto load_pre = [&]() {
+    const uint32_t c = next + lane;
+    if (c < NC) pre = a.rec[c];
+    else { pre.e = 0xFFFFFFFFu; pre.s = 0; }
+  };
+  auto load_ps = [&]() {
+    if (next + lane < NC) ps = sess[pre.s];
+  };
+  load_pre();
+  load_ps();
 
   auto recompute_L = [&]() {
     int64_t s = 0;
@@ -74,11 +134,11 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     for (uint32_t i = 0; i < len; ++i) {
       uint32_t x = qc[i];
       if (x & STARTED) continue;
-      uint32_t s = v.call_sess[x & CMASK];
-      if (a.moved[s]) continue;
+      uint32_t s = x & CMASK;
+      if (moved[s]) continue;
       bool busy = false;
       for (uint32_t j = 0; j < len; ++j)
-        if ((qc[j] & STARTED) && v.call_sess[qc[j] & CMASK] == s) { busy = true; break; }
+        if ((qc[j] & STARTED) && (qc[j] & CMASK) == s) { busy = true; break; }
       if (!busy) return (int32_t)s;
     }
     return -1;
@@ -86,12 +146,12 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
 
   while (true) {
     bool any = __ballot_sync(0xffffffffu, act_lane && len > 0) != 0;
-    if (next >= v.n_calls && !any) break;
+    if (next >= NC && !any) break;
     const int64_t Te = (int64_t)e * E;
     bool got = false;
     // ---------------- P1 service: the first kappa calls progress by one epoch ----------------
     if (act_lane) {
-      int64_t served = 0;
+      int64_t served = 0, Ls = 0;
       uint32_t k = 0;
       for (uint32_t i = 0; i < len; ++i) {
         uint32_t x = qc[i], r = qr[i];
@@ -100,13 +160,14 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           r -= d;
           served += d;
           x |= STARTED;
-          if (r == 0) { a.moved[v.call_sess[x & CMASK]] = 0; continue; }
+          if (r == 0) { moved[x & CMASK] = 0; continue; }
         }
         qc[k] = x; qr[k] = r; ++k;
+        Ls += min((int64_t)r, E);
       }
       len = k;
       idle = served == 0 ? idle + 1 : 0;
-      recompute_L();
+      L = Ls;
     }
     __syncwarp();
     // ---------------- P2 steal: idle thief AND load-ratio guard (P:361, P:766(a)) ----------------
@@ -114,6 +175,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     bool unst = false;
     if (act_lane) for (uint32_t i = 0; i < len; ++i) if (!(qc[i] & STARTED)) { unst = true; break; }
     if (thieves && __ballot_sync(0xffffffffu, unst)) {
+      bool stole = false;
       while (thieves) {
         const uint32_t th = __ffs(thieves) - 1;
         thieves &= thieves - 1;
@@ -130,7 +192,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           uint32_t k = 0, m = 0;
           for (uint32_t i = 0; i < len; ++i) {
             uint32_t x = qc[i];
-            if (v.call_sess[x & CMASK] == (uint32_t)s) {
+            if ((x & CMASK) == (uint32_t)s) {
               if (m < 64) { xfer_c[m] = x; xfer_r[m] = qr[i]; }
               ++m;
             } else { qc[k] = x; qr[k] = qr[i]; ++k; }
@@ -152,46 +214,43 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           got = true;
         }
         if (lane == 0) {
-          uint32_t ty = v.styp[s];
-          if (!a.fin[s]) {  // s is counted at its current affinity node
-            const int32_t ao = a.aff[s];
+          SessRec sr = sess[s];
+          const uint32_t ty = v.styp[s];
+          if (!(sr.ttlf & S_FIN)) {  // s is counted at its current affinity node
+            const int32_t ao = sr.aff;
             cnt[ao][ty]--; act_tot[ao]--; cnt[th][ty]++; act_tot[th]++;
           }
-          a.aff[s] = (int32_t)th;
-          a.moved[s] = 1;
+          sr.aff = (int32_t)th;
+          sess[s] = sr;
+          moved[s] = 1;
           if (n_mig < a.mig_cap) a.migs[n_mig] = Mig{(uint32_t)e, (uint32_t)s, vv, th};
           else errf |= 2u;
           ++n_mig;
           ++steals;
         }
+        stole = true;
         __syncwarp();
       }
+      if (stole) load_ps();  // affinities of prefetched sessions may have changed
     }
     // ---------------- P3 route the calls admitted at T_e (eq:routing) ----------------
-    while (next < v.n_calls && v.ecall[next] == e) {
+    while (next < NC && __shfl_sync(0xffffffffu, pre.e, 0) == (uint32_t)e) {
       const uint32_t c = next + lane;
-      const bool valid = c < v.n_calls && v.ecall[c] == e;
+      const bool valid = c < NC && pre.e == (uint32_t)e;
       const uint32_t nb = __popc(__ballot_sync(0xffffffffu, valid));
-      uint32_t s = 0, vc = 0, ty = 0, newt = 0, prompt = 0, outt = 0;
-      bool lastc = false, termc = false;
-      int64_t tendc = 0, ttlc = 0;
-      int32_t aff = -1, lc = -1;
-      bool fin = false, term_lv = true;
-      int64_t tend_lv = 0, ttl_lv = 0;
-      if (valid) {
-        s = v.call_sess[c]; vc = v.call_v[c]; ty = v.styp[s];
-        newt = v.call_new[c]; prompt = v.call_prompt[c]; outt = v.call_out[c];
-        lastc = v.call_last[c]; termc = v.term[vc]; tendc = v.tend[c]; ttlc = v.ttl[vc];
-        aff = a.aff[s]; lc = a.last_c[s]; fin = a.fin[s];
-        if (lc >= 0) { uint32_t lv = v.call_v[lc]; term_lv = v.term[lv]; tend_lv = v.tend[lc]; ttl_lv = v.ttl[lv]; }
-      }
+      const uint32_t s = pre.s, ty = pre.tyf & 0xFFFFu;
+      const bool f_new_l = (pre.tyf & F_FNEW) != 0;
+      int32_t aff = valid ? ps.aff : -1;
+      bool fin = valid && (ps.ttlf & S_FIN);
+      bool term_lv = !valid || (ps.ttlf & S_TERM);
+      int64_t tend_lv = ps.tend_lv, ttl_lv = ps.ttlf & (S_FIN - 1u);
       const uint32_t same = __match_any_sync(0xffffffffu, valid ? s : 0xFFFFFFFFu);
       for (uint32_t i = 0; i < nb; ++i) {
         // lane i's view of its session state
         const int32_t ws = __shfl_sync(0xffffffffu, aff, i);
-        bool cached_i = (aff >= 0) && !term_lv && (Te - tend_lv <= ttl_lv);   // Alg. 1 with m = 0
+        const bool cached_i = (aff >= 0) && !term_lv && (Te - tend_lv <= ttl_lv);   // Alg. 1 with m = 0
         const bool cached = __shfl_sync(0xffffffffu, cached_i, i);
-        int64_t Lws = __shfl_sync(0xffffffffu, (long long)L, ws >= 0 ? ws : 0);
+        const int64_t Lws = __shfl_sync(0xffffffffu, (long long)L, ws >= 0 ? ws : 0);
         uint32_t w;
         if (cached && 1000 * Lws < (int64_t)a.theta_pm * (int64_t)K * E) {
           w = (uint32_t)ws;
@@ -208,18 +267,15 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           }
           w = kW;
         }
-        const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
-        const uint32_t si = __shfl_sync(0xffffffffu, s, i);
+        const bool use_cached = cached && (int32_t)w == ws;
+        const uint32_t omega = __shfl_sync(0xffffffffu, use_cached ? pre.om_cached : pre.om_full, i);
         const uint32_t tyi = __shfl_sync(0xffffffffu, ty, i);
+        const uint32_t si = __shfl_sync(0xffffffffu, s, i);
         const bool fin_old = __shfl_sync(0xffffffffu, fin, i);
-        const bool f_new = __shfl_sync(0xffffffffu, (int)(lastc || termc), i);
-        const uint32_t pf = __shfl_sync(0xffffffffu, (cached && (int32_t)w == ws) ? newt : prompt, i);
-        const uint32_t oi = __shfl_sync(0xffffffffu, outt, i);
-        const int64_t omega = ceil_div64((int64_t)pf * 1000000, v.prefill_tok_s) +
-                              ceil_div64((int64_t)oi * 1000000, v.decode_tok_s);
+        const bool f_new = __shfl_sync(0xffffffffu, f_new_l, i);
         if (lane == w) {
           if (len >= Q) atomicOr(&errf, 1u);
-          else { qc[len] = ci; qr[len] = (uint32_t)omega; ++len; L += min(omega, E); }
+          else { qc[len] = si; qr[len] = omega; ++len; L += min((int64_t)omega, E); }
           got = true;
         }
         if (lane == 0) {
@@ -227,24 +283,28 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           if (ws >= 0 && !fin_old) { cnt[ws][tyi]--; act_tot[ws]--; }
           if (!f_new) { cnt[w][tyi]++; act_tot[w]++; }
         }
-        if (lane == i) a.node_of[ci] = (uint8_t)w;
+        if (lane == i) a.node_of[c] = (uint8_t)w;
         // forward the post-call state to later lanes of the same session in this batch
-        const uint32_t vci = __shfl_sync(0xffffffffu, vc, i);
-        const int64_t tendi = __shfl_sync(0xffffffffu, (long long)tendc, i);
-        const int64_t ttli = __shfl_sync(0xffffffffu, (long long)ttlc, i);
-        const bool termi = __shfl_sync(0xffffffffu, (int)termc, i);
-        if (valid && (lane == i || (lane > i && si == s && ((same >> i) & 1u)))) {
-          aff = (int32_t)w; lc = (int32_t)ci; fin = f_new;
+        const int64_t tendi = __shfl_sync(0xffffffffu, (long long)pre.tend, i);
+        const uint32_t ttli = __shfl_sync(0xffffffffu, pre.ttl, i);
+        const bool termi = __shfl_sync(0xffffffffu, (int)((pre.tyf & F_TERM) != 0), i);
+        if (valid && (lane == i || (lane > i && ((same >> i) & 1u)))) {
+          aff = (int32_t)w; fin = f_new;
           term_lv = termi; tend_lv = tendi; ttl_lv = ttli;
         }
-        (void)vci;
         __syncwarp();
       }
       // the last lane of each session in the batch publishes the session state
       const uint32_t later = same & ~((2u << lane) - 1u);
-      if (valid && later == 0) { a.aff[s] = aff; a.last_c[s] = lc; a.fin[s] = fin; }
+      if (valid && later == 0) {
+        SessRec r{aff, (uint32_t)ttl_lv | (fin ? S_FIN : 0u) | (term_lv ? S_TERM : 0u), tend_lv};
+        sess[s] = r;
+      }
       __syncwarp();
       next += nb;
+      load_pre();
+      __syncwarp();
+      load_ps();
     }
     // ---------------- act(w, a) log for nodes that received records at this boundary ----------------
     const uint32_t gm = __ballot_sync(0xffffffffu, act_lane && got);
@@ -265,25 +325,26 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     // ---------------- closed-form advance over service-only epochs ----------------
     const bool all_fit = __ballot_sync(0xffffffffu, act_lane && len > K) == 0;
     if (all_fit) {
-      uint64_t e_adm = next < v.n_calls ? (uint64_t)v.ecall[next] : UINT64_MAX;
+      const uint32_t e_next = __shfl_sync(0xffffffffu, pre.e, 0);
       uint64_t k;
-      if (e_adm == UINT64_MAX) {
+      if (next >= NC) {
         int64_t mx = 0;
         if (act_lane) for (uint32_t i = 0; i < len; ++i) mx = max(mx, (int64_t)qr[i]);
         mx = -warp_min64(-mx);
         k = (uint64_t)ceil_div64(mx, E);
       } else {
-        k = e_adm - 1 - e;
+        k = (uint64_t)e_next - 1 - e;
       }
       if (k > 0 && act_lane) {
         const int64_t budget = (int64_t)k * E;
-        int64_t mx = 0;
+        int64_t mx = 0, Ls = 0;
         uint32_t kk = 0;
         for (uint32_t i = 0; i < len; ++i) {
           int64_t r = qr[i];
           mx = max(mx, r);
-          if (r <= budget) { a.moved[v.call_sess[qc[i] & CMASK]] = 0; continue; }
+          if (r <= budget) { moved[qc[i] & CMASK] = 0; continue; }
           qc[kk] = qc[i] | STARTED; qr[kk] = (uint32_t)(r - budget); ++kk;
+          Ls += min(r - budget, E);
         }
         if (len == 0) idle += (int64_t)k;
         else {
@@ -291,7 +352,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           idle = m >= k ? 0 : (int64_t)(k - m);
         }
         len = kk;
-        recompute_L();
+        L = Ls;
       }
       e += k;
     }
@@ -307,15 +368,32 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   }
 }
 
+__global__ void k_sess_init(SessRec* s, uint8_t* moved, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    s[i] = SessRec{-1, 0u, 0ll};
+    moved[i] = 0;
+  }
+}
+
+unsigned grid_for(uint64_t n, int threads = NTHREADS) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148u * 64u) g = 148u * 64u;
+  return (unsigned)g;
+}
+
 }  // namespace
 
 saga_status run_placement(saga_trace* t) {
   const TraceView& v = t->v;
   const uint32_t W = v.n_nodes;
-  size_t max_smem = 200 * 1024;
-  uint32_t qcap = (uint32_t)(max_smem / (8ull * W));
+  const size_t max_smem = 200 * 1024;
+  const size_t sess_bytes = ((size_t)v.n_sessions * (sizeof(SessRec) + 1) + 15) & ~(size_t)15;
+  // sessions in shared memory if that still leaves >= 256 queue slots per node
+  const bool ss = sess_bytes + 256ull * 8 * W <= max_smem;
+  uint32_t qcap = (uint32_t)((max_smem - (ss ? sess_bytes : 0)) / (8ull * W));
   if (qcap > 65536) qcap = 65536;
-  size_t smem = size_t(qcap) * W * 8;
+  const size_t smem = (ss ? sess_bytes : 0) + size_t(qcap) * W * 8;
   uint32_t mig_cap = v.n_calls + v.n_sessions + 64;
   uint32_t act_cap = v.n_calls + mig_cap + 64;
   t->node_of = dalloc<uint8_t>(t, v.n_calls);
@@ -323,28 +401,33 @@ saga_status run_placement(saga_trace* t) {
   t->act = dalloc<ActRec>(t, act_cap);
   uint32_t* out_n = dalloc<uint32_t>(t, 4);
   unsigned long long* out_stats = dalloc<unsigned long long>(t, 2);
-  int32_t* aff = dalloc<int32_t>(t, v.n_sessions);
-  int32_t* lastc = dalloc<int32_t>(t, v.n_sessions);
-  uint8_t* moved = dalloc<uint8_t>(t, v.n_sessions);
-  uint8_t* fin = dalloc<uint8_t>(t, v.n_sessions);
-  if (!t->node_of || !t->migs || !t->act || !out_n || !out_stats || !aff || !lastc || !moved || !fin) {
+  CallRec* rec = dalloc<CallRec>(t, v.n_calls);
+  SessRec* sess = ss ? nullptr : dalloc<SessRec>(t, v.n_sessions);
+  uint8_t* moved = ss ? nullptr : dalloc<uint8_t>(t, v.n_sessions);
+  if (!t->node_of || !t->migs || !t->act || !out_n || !out_stats || !rec || (!ss && (!sess || !moved))) {
     set_error("saga_load_trace: out of device memory (placement)");
     return SAGA_ERR_OOM;
   }
-  SAGA_CK(cudaMemsetAsync(aff, 0xFF, size_t(v.n_sessions) * 4, t->stream));
-  SAGA_CK(cudaMemsetAsync(lastc, 0xFF, size_t(v.n_sessions) * 4, t->stream));
-  SAGA_CK(cudaMemsetAsync(moved, 0, v.n_sessions, t->stream));
-  SAGA_CK(cudaMemsetAsync(fin, 0, v.n_sessions, t->stream));
   SAGA_CK(cudaMemsetAsync(out_n, 0, 16, t->stream));
   PlaceArgs a{};
   a.v = v;
+  a.rec = rec;
   a.kappa = t->pcfg.kappa; a.theta_pm = t->pcfg.theta_pm; a.rmax_pm = t->pcfg.rmax_pm; a.qcap = qcap;
   a.t_idle_us = t->pcfg.t_idle_us; a.seed = t->pcfg.seed;
   a.node_of = t->node_of; a.migs = t->migs; a.mig_cap = mig_cap; a.act = t->act; a.act_cap = act_cap;
-  a.out_n = out_n; a.out_stats = out_stats; a.aff = aff; a.last_c = lastc; a.moved = moved; a.fin = fin;
-  SAGA_CK(cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  a.out_n = out_n; a.out_stats = out_stats; a.sess_g = sess; a.moved_g = moved;
   prof_begin(SAGA_PROF_PLACE, t->stream);
-  k_place<<<1, 32, smem, t->stream>>>(a);
+  if (v.n_calls) k_call_rec<<<grid_for(v.n_calls), NTHREADS, 0, t->stream>>>(v, rec);
+  count_launch();
+  if (ss) {
+    SAGA_CK(cudaFuncSetAttribute(k_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_place<true><<<1, 32, smem, t->stream>>>(a);
+  } else {
+    k_sess_init<<<grid_for(v.n_sessions), NTHREADS, 0, t->stream>>>(sess, moved, v.n_sessions);
+    count_launch();
+    SAGA_CK(cudaFuncSetAttribute(k_place<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_place<false><<<1, 32, smem, t->stream>>>(a);
+  }
   prof_end(SAGA_PROF_PLACE, t->stream);
   count_launch();
   SAGA_CK_LAUNCH();

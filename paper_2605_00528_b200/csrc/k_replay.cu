@@ -88,7 +88,11 @@ struct ReplayArgs {
   // per-CTA scratch (strides in elements)
   uint8_t* scratch;
   uint64_t cta_bytes;
-  uint64_t o_res, o_bits, o_c1, o_c2, o_dbits, o_dc1, o_dc2, o_cnt, o_list0, o_list1, o_lkp, o_kbuf, o_sst;
+  uint64_t o_res, o_bits, o_c1, o_dbits, o_dc1, o_cnt, o_list0, o_list1, o_lkp, o_kbuf, o_vl, o_sst;
+  uint32_t n2N_max, n2L_max;   // c2 entries of the two bitmaps (dynamic shared memory)
+  uint32_t dyn_c1;             // the c1 arrays are in dynamic shared memory too
+  uint32_t dyn_words;          // dynamic shared memory size in 32-bit words
+  unsigned long long* item_cyc;  // optional per-item SM cycles (SAGA_REPLAY_TRACE)
   uint32_t* work;
   uint32_t* err;
 };
@@ -97,8 +101,10 @@ struct Smem {
   BlockScratch<RT> b;
   uint32_t hist[H1];
   uint32_t res_j, res_rem, thr, item;
-  uint32_t n_app, n_piv;
+  uint32_t hb_j2, hb_j1;
+  uint32_t n_app, n_piv, n_vict;
   uint32_t ilo, ihi;
+  uint32_t tot_dead, tot_pend;  // BELADY: set bits of the two hierarchical bitmaps
 };
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
@@ -108,18 +114,31 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
 }
 
 // arr[lo..hi) scanned from hi-1 downwards: j with sum(arr[j+1..hi)) < k <= sum(arr[j..hi)) and
-// rem = k - sum(arr[j+1..hi)).  Requires 1 <= k <= sum(arr[lo..hi)).  Block-wide.
+// rem = k - sum(arr[j+1..hi)).  Requires 1 <= k <= sum(arr[lo..hi)).  Block-wide; each thread
+// takes IT consecutive entries per round, so up to RT*IT entries cost one collective.
+template <int IT>
 __device__ void find_level(const uint32_t* arr, uint32_t lo, uint32_t hi, uint32_t k, uint32_t& j, uint32_t& rem,
-                           Smem& sm) {
+                           Smem& sm, Par& par) {
   uint32_t carry = 0;
-  for (uint32_t base = 0; base < hi - lo; base += RT) {
-    const uint32_t t = base + threadIdx.x;
-    const bool in = t < hi - lo;
-    const uint32_t idx = hi - 1 - t;
-    const uint32_t v = in ? arr[idx] : 0u;
+  const uint32_t n = hi - lo;
+  for (uint32_t base = 0; base < n; base += RT * IT) {
+    uint32_t val[IT], sum = 0;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const uint32_t t = base + threadIdx.x * IT + i;
+      val[i] = t < n ? arr[hi - 1 - t] : 0u;
+      sum += val[i];
+    }
     uint32_t tot;
-    const uint32_t ex = block_excl_scan<RT>(v, &tot, sm.b.u32);
-    if (in && carry + ex < k && k <= carry + ex + v) { sm.res_j = idx; sm.res_rem = k - carry - ex; }
+    const uint32_t ex = block_excl_scan<RT>(sum, &tot, sm.b, par);
+    uint32_t c = carry + ex;
+    if (c < k && k <= c + sum) {
+#pragma unroll
+      for (int i = 0; i < IT; ++i) {
+        if (c < k && k <= c + val[i]) { sm.res_j = hi - 1 - (base + threadIdx.x * IT + i); sm.res_rem = k - c; }
+        c += val[i];
+      }
+    }
     carry += tot;
     if (carry >= k) break;
   }
@@ -154,16 +173,28 @@ __device__ __forceinline__ void hb_update_warp(const HB& h, bool act, uint32_t i
   }
 }
 
-// number of set bits (block-wide sum of c2)
-__device__ uint32_t hb_total(const HB& h, Smem& sm) {
-  uint32_t s = 0;
-  for (uint32_t i = threadIdx.x; i < h.n2; i += RT) s += h.c2[i];
-  return block_reduce<RT, uint32_t>(s, Add(), sm.b.u32);
+// Warp-collective (all lanes call): each lane appends idx(b) | tag for every set bit b of
+// `bits` (bit b of word wi is index wi * 32 + b) to the victim list.
+__device__ __forceinline__ void emit_bits(uint32_t* vlist, uint32_t* n_vict, uint32_t wi, uint32_t bits, uint32_t tag) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = __popc(bits);
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+  if (tot == 0) return;
+  uint32_t b0 = 0;
+  if (lane == 31) b0 = atomicAdd(n_vict, tot);
+  b0 = __shfl_sync(0xffffffffu, b0, 31) + x - c;
+  for (uint32_t y = bits; y; y &= y - 1) vlist[b0++] = (wi * 32u + (uint32_t)(__ffs(y) - 1)) | tag;
 }
 
-// take (clear and emit) every set bit with index >= T, starting at c1 block j1 of c2 block j2
-template <class Emit>
-__device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, Emit& emit) {
+// take (clear and list) every set bit with index >= T, starting at c1 block j1 of c2 block j2
+__device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, uint32_t* vlist, uint32_t* n_vict,
+                             uint32_t tag) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t tw = T >> 5;
   for (uint32_t jb = j2; jb < h.n2; ++jb) {
@@ -181,10 +212,8 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
         const uint32_t m = wi > tw ? 0xffffffffu : (wi == tw ? ~((1u << (T & 31)) - 1u) : 0u);
         const uint32_t wv = h.bits[wi];
         const uint32_t tk = wv & m;
-        if (tk) {
-          h.bits[wi] = wv & ~m;
-          for (uint32_t x = tk; x; x &= x - 1) emit(wi * 32u + (uint32_t)(__ffs(x) - 1));
-        }
+        if (tk) h.bits[wi] = wv & ~m;
+        emit_bits(vlist, n_vict, wi, tk, tag);
         const uint32_t n = warp_sum(__popc(tk));
         if (lane == 0 && n) { h.c1[c1i] -= n; atomicSub(&h.c2[jb], n); }
       }
@@ -192,40 +221,82 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
   }
 }
 
-// take the k highest set bits (1 <= k <= total)
-template <class Emit>
-__device__ void hb_take_top(const HB& h, uint32_t k, Emit& emit, Smem& sm) {
-  uint32_t j2, r2, j1, r1;
-  find_level(h.c2, 0, h.n2, k, j2, r2, sm);
-  find_level(h.c1, j2 * 1024u, j2 * 1024u + 1024u, r2, j1, r1, sm);
+// take the k highest set bits (1 <= k <= total).  The threshold is found by warp 0 alone
+// (c2 level, then the 1024 c1 entries of the pivot c2 block as 32 lanes x 32, then 32 words).
+__device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t tag, Smem& sm) {
   if (threadIdx.x < 32) {
     const uint32_t lane = threadIdx.x;
-    const uint32_t wi = j1 * 32u + (31u - lane);  // lane 0 = highest word of the block
-    const uint32_t wv = h.bits[wi];
-    const uint32_t c = __popc(wv);
-    uint32_t x = c;
+    // c2 level
+    uint32_t carry = 0, j2 = 0, r2 = 0;
+    for (uint32_t base = 0; base < h.n2; base += 32) {
+      const uint32_t idx = h.n2 - 1 - (base + lane);
+      const uint32_t v = base + lane < h.n2 ? h.c2[idx] : 0u;
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+      }
+      const uint32_t hit = __ballot_sync(0xffffffffu, carry + x - v < k && k <= carry + x);
+      if (hit) {
+        const int l = __ffs(hit) - 1;
+        j2 = __shfl_sync(0xffffffffu, idx, l);
+        r2 = k - __shfl_sync(0xffffffffu, carry + x - v, l);
+        break;
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    // c1 level: lane l owns entries [top - 32 l - 31, top - 32 l] of block j2
+    const uint32_t b0 = j2 * 1024u + 1024u - 32u * (lane + 1);
+    const uint4* c4 = reinterpret_cast<const uint4*>(h.c1 + b0);
+    uint32_t e[32], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 t = c4[q];
+      e[4 * q] = t.x; e[4 * q + 1] = t.y; e[4 * q + 2] = t.z; e[4 * q + 3] = t.w;
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) sum += e[q];
+    uint32_t x = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= (uint32_t)o) x += y;
     }
-    if (x - c < r1 && r1 <= x) {
-      uint32_t need = r1 - (x - c), w2 = wv;
+    const uint32_t hit = __ballot_sync(0xffffffffu, x - sum < r2 && r2 <= x);
+    const int L = __ffs(hit) - 1;
+    uint32_t j1 = 0, r1 = 0;
+    if ((int)lane == L) {
+      uint32_t c = x - sum;
+#pragma unroll
+      for (int q = 31; q >= 0; --q) {
+        if (c < r2 && r2 <= c + e[q]) { j1 = b0 + (uint32_t)q; r1 = r2 - c; }
+        c += e[q];
+      }
+    }
+    j1 = __shfl_sync(0xffffffffu, j1, L);
+    r1 = __shfl_sync(0xffffffffu, r1, L);
+    // word level
+    const uint32_t wi = j1 * 32u + (31u - lane);  // lane 0 = highest word of the block
+    const uint32_t wv = h.bits[wi];
+    const uint32_t cw = __popc(wv);
+    uint32_t xw = cw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, xw, o);
+      if (lane >= (uint32_t)o) xw += y;
+    }
+    if (xw - cw < r1 && r1 <= xw) {
+      uint32_t need = r1 - (xw - cw), w2 = wv;
       int b = 31 - __clz(w2);
       while (--need) { w2 &= ~(1u << b); b = 31 - __clz(w2); }
       sm.thr = wi * 32u + (uint32_t)b;
+      sm.hb_j2 = j2;
+      sm.hb_j1 = j1;
     }
   }
   __syncthreads();
-  const uint32_t T = sm.thr;
-  hb_take_from(h, j2, j1, T, emit);
-  __syncthreads();
-}
-
-template <class Emit>
-__device__ void hb_take_all(const HB& h, Emit& emit) {
-  hb_take_from(h, 0, 0, 0, emit);
-  __syncthreads();
+  hb_take_from(h, sm.hb_j2, sm.hb_j1, sm.thr, vlist, &sm.n_vict, tag);
 }
 
 __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
@@ -261,31 +332,23 @@ __device__ __forceinline__ uint32_t owner_size(const TraceView& v, const uint32_
   return __ldg(&v.ci_size[c1 ? c1 - 1 : 0]);
 }
 
-// per-thread victim bookkeeping
-struct Vict {
-  uint32_t* res_pos;
-  unsigned long long hash;
-  uint32_t n, np;
-  uint64_t eh;  // e << 32
-  __device__ __forceinline__ void operator()(uint32_t lid) {
-    res_pos[lid] = NONE;
-    hash += splitmix64(eh | lid);
-    ++n;
-  }
-};
+constexpr uint32_t VT_LID = 0x80000000u;  // victim-list tag: the entry is a local id, else a position
+constexpr int UNR = 4;                    // record chunks whose loads are issued together (R2 / R4)
 
 __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
   __shared__ Smem sm;
   __shared__ long long s_ctr[SAGA_NCOUNT];
+  extern __shared__ __align__(16) uint32_t dyn[];  // c2 (+ c1) counts / AEG unit counts
+  Par par;
   const TraceView& v = a.v;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* base = a.scratch + (uint64_t)blockIdx.x * a.cta_bytes;
   uint32_t* res_pos = reinterpret_cast<uint32_t*>(base + a.o_res);
   uint32_t* alive = reinterpret_cast<uint32_t*>(base + a.o_bits);   // AEG / EVICT_ALL (aliases pend.bits)
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(base + a.o_cnt);
   uint32_t* lists[2] = {reinterpret_cast<uint32_t*>(base + a.o_list0), reinterpret_cast<uint32_t*>(base + a.o_list1)};
   uint32_t* lkp = reinterpret_cast<uint32_t*>(base + a.o_lkp);
   uint64_t* kbuf = reinterpret_cast<uint64_t*>(base + a.o_kbuf);
+  uint32_t* vlist = reinterpret_cast<uint32_t*>(base + a.o_vl);
   uint32_t* sstate = reinterpret_cast<uint32_t*>(base + a.o_sst);
 
   while (true) {
@@ -294,6 +357,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
     const uint32_t it = sm.item;
     __syncthreads();
     if (it >= a.n_items) break;
+    const long long t_start = clock64();
     const uint32_t packed = a.items[it];
     const uint32_t pi = packed >> 28, ci = (packed >> 12) & 0xFFFFu, ni = packed & 0xFFFu;
     const uint32_t pol = a.pol[pi];
@@ -302,34 +366,36 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
     const NodeArr nd = a.nodes[w];
     const bool belady = pol == SAGA_POLICY_BELADY;
     const bool aeg = pol == SAGA_POLICY_AEG;
-    const uint32_t n2N = (uint32_t)((nd.N + (1u << 20) - 1) >> 20) + 0u;
-    const uint32_t n2L = (nd.n_local + (1u << 20) - 1) >> 20;
-    HB pend{reinterpret_cast<uint32_t*>(base + a.o_bits), reinterpret_cast<uint32_t*>(base + a.o_c1),
-            reinterpret_cast<uint32_t*>(base + a.o_c2), n2N > 0 ? n2N : 1u};
-    HB dead{reinterpret_cast<uint32_t*>(base + a.o_dbits), reinterpret_cast<uint32_t*>(base + a.o_dc1),
-            reinterpret_cast<uint32_t*>(base + a.o_dc2), n2L > 0 ? n2L : 1u};
+    const uint32_t n2N = max(1u, (uint32_t)((nd.N + (1u << 20) - 1) >> 20));
+    const uint32_t n2L = max(1u, (nd.n_local + (1u << 20) - 1) >> 20);
+    // count arrays: c2 always in shared memory, c1 there too when it fits (a.dyn_c1)
+    uint32_t* c2N = dyn;
+    uint32_t* c2L = dyn + a.n2N_max;
+    uint32_t* c1N = a.dyn_c1 ? dyn + ((a.n2N_max + a.n2L_max + 3u) & ~3u) : reinterpret_cast<uint32_t*>(base + a.o_c1);
+    uint32_t* c1L = a.dyn_c1 ? c1N + a.n2N_max * 1024u : reinterpret_cast<uint32_t*>(base + a.o_dc1);
+    HB pend{reinterpret_cast<uint32_t*>(base + a.o_bits), c1N, c2N, n2N};
+    HB dead{reinterpret_cast<uint32_t*>(base + a.o_dbits), c1L, c2L, n2L};
+    // AEG / EVICT_ALL unit counts: in shared memory when they fit
+    uint32_t* cnt = (a.dyn_words >= nd.n_units) ? dyn : reinterpret_cast<uint32_t*>(base + a.o_cnt);
     // ---- reset the item state ----
     {
-      uint4 ones = make_uint4(NONE, NONE, NONE, NONE), zero = make_uint4(0, 0, 0, 0);
+      const uint4 ones = make_uint4(NONE, NONE, NONE, NONE), zero = make_uint4(0, 0, 0, 0);
       uint4* r4 = reinterpret_cast<uint4*>(res_pos);
       for (uint32_t i = threadIdx.x; i < (nd.n_local + 3) / 4; i += RT) r4[i] = ones;
-      const uint32_t nbw = pend.n2 * 32768u;
       uint4* b4 = reinterpret_cast<uint4*>(pend.bits);
-      for (uint32_t i = threadIdx.x; i < nbw / 4; i += RT) b4[i] = zero;
+      for (uint32_t i = threadIdx.x; i < n2N * 8192u; i += RT) b4[i] = zero;
       if (belady) {
-        uint4* c4 = reinterpret_cast<uint4*>(pend.c1);
-        for (uint32_t i = threadIdx.x; i < pend.n2 * 256u; i += RT) c4[i] = zero;
-        for (uint32_t i = threadIdx.x; i < pend.n2; i += RT) pend.c2[i] = 0;
+        for (uint32_t i = threadIdx.x; i < n2N * 1024u; i += RT) c1N[i] = 0;
+        for (uint32_t i = threadIdx.x; i < n2L * 1024u; i += RT) c1L[i] = 0;
+        for (uint32_t i = threadIdx.x; i < a.n2N_max + a.n2L_max; i += RT) dyn[i] = 0;
         uint4* d4 = reinterpret_cast<uint4*>(dead.bits);
-        for (uint32_t i = threadIdx.x; i < dead.n2 * 8192u; i += RT) d4[i] = zero;
-        uint4* dc4 = reinterpret_cast<uint4*>(dead.c1);
-        for (uint32_t i = threadIdx.x; i < dead.n2 * 256u; i += RT) dc4[i] = zero;
-        for (uint32_t i = threadIdx.x; i < dead.n2; i += RT) dead.c2[i] = 0;
+        for (uint32_t i = threadIdx.x; i < n2L * 8192u; i += RT) d4[i] = zero;
       } else {
         for (uint32_t i = threadIdx.x; i < nd.n_units; i += RT) cnt[i] = 0;
       }
       if (aeg) for (uint32_t i = threadIdx.x; i < v.n_sessions; i += RT) sstate[i] = 0;
       if (threadIdx.x < SAGA_NCOUNT) s_ctr[threadIdx.x] = 0;
+      if (threadIdx.x == 0) { sm.tot_dead = 0; sm.tot_pend = 0; }
       __syncthreads();
     }
     uint32_t S = 0;       // |S| (uniform)
@@ -371,13 +437,14 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           ++nrm;
           if (belady) {
             const uint32_t q = nd.nxt[p];
-            if (q == INF32) hb_clear(dead, l); else hb_clear(pend, q);
+            if (q == INF32) { hb_clear(dead, l); atomicSub(&sm.tot_dead, 1u); }
+            else { hb_clear(pend, q); atomicSub(&sm.tot_pend, 1u); }
           } else {
             atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
             atomicSub(&cnt[nd.u_of[p] & UMASK], 1u);
           }
         }
-        nrm = block_reduce<RT, uint32_t>(nrm, Add(), sm.b.u32);
+        nrm = block_reduce<RT, uint32_t>(nrm, Add(), sm.b, par);
         S -= nrm;
         c_inv += nrm;  // uniform
       }
@@ -385,46 +452,48 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       const uint64_t P0 = nd.ev_pos[j], P1 = nd.ev_pos[j + 1];
       if (P0 == P1) continue;    // only empty record groups (the oracle skips the epoch)
       __syncthreads();
+      if (threadIdx.x == 0) sm.n_vict = 0;
       // ---- R2: |A|, new = |A \ S|; hits / misses; in-flight blocks leave the index ----
       uint32_t nA = 0, nnew = 0;
       uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_comp = 0, t_regen = 0;
-      for (uint64_t wb = (P0 & ~31ull) + (uint64_t)wid * 32u; wb < P1; wb += RT) {
-        const uint64_t pb = wb + lane;
-        const bool in = pb >= P0 && pb < P1;
-        uint32_t lf = 0, uo = 0, lid = 0;
-        bool first = false, resident = false;
-        uint32_t rp = NONE;
-        if (in) {
-          lf = nd.lidf[pb];
-          uo = nd.u_of[pb];
-          lid = lf & LID_MASK;
-          first = !(lf & LID_NFIE);
-          const bool mig = (uo & KIND_MIG) != 0;
-          if (first) {
-            ++nA;
-            rp = res_pos[lid];
-            resident = rp != NONE;
-            if (!resident) {
-              ++nnew;
-              if (mig) ++t_mmiss; else { ++t_miss; if (!(lf & LID_FTN)) ++t_regen; }
-              if (lf & LID_FTN) ++t_comp;
+      for (uint64_t wb = (P0 & ~31ull) + (uint64_t)wid * 32u; wb < P1; wb += (uint64_t)RT * UNR) {
+        uint32_t lf[UNR], uo[UNR], rp[UNR];
+        bool in[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint64_t pb = wb + (uint64_t)u * RT + lane;
+          in[u] = pb >= P0 && pb < P1;
+          lf[u] = in[u] ? nd.lidf[pb] : 0u;
+          uo[u] = in[u] ? nd.u_of[pb] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) rp[u] = (in[u] && !(lf[u] & LID_NFIE)) ? res_pos[lf[u] & LID_MASK] : NONE;
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const bool first = in[u] && !(lf[u] & LID_NFIE);
+          const bool resident = first && rp[u] != NONE;
+          const bool mig = (uo[u] & KIND_MIG) != 0;
+          if (in[u]) {
+            if (first && !resident) {
+              ++nA; ++nnew;
+              if (mig) ++t_mmiss; else { ++t_miss; if (!(lf[u] & LID_FTN)) ++t_regen; }
+              if (lf[u] & LID_FTN) ++t_comp;
             } else {
+              if (first) ++nA;
               if (mig) ++t_mhit; else ++t_hit;
             }
-          } else {
-            if (mig) ++t_mhit; else ++t_hit;
           }
-        }
-        if (belady) {
-          hb_update_warp(pend, in && first && resident, (uint32_t)pb, false);
-        } else if (in && first && resident) {
-          atomicAnd(&alive[rp >> 5], ~(1u << (rp & 31)));
-          atomicSub(&cnt[nd.u_of[rp] & UMASK], 1u);
+          if (belady) {
+            hb_update_warp(pend, resident, (uint32_t)(wb + (uint64_t)u * RT + lane), false);
+          } else if (resident) {
+            atomicAnd(&alive[rp[u] >> 5], ~(1u << (rp[u] & 31)));
+            atomicSub(&cnt[nd.u_of[rp[u]] & UMASK], 1u);
+          }
         }
       }
       {
         const unsigned long long pk = block_reduce<RT, unsigned long long>(
-            ((unsigned long long)nA << 32) | nnew, Add(), sm.b.u64);
+            ((unsigned long long)nA << 32) | nnew, Add(), sm.b, par);
         nA = (uint32_t)(pk >> 32);
         nnew = (uint32_t)pk;
       }
@@ -436,46 +505,51 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       // ---- R3: evict the k largest keys among cand = S \ A ----
       if (kk > 0) {
         const uint32_t k = (uint32_t)kk;
-        Vict vc{res_pos, 0ull, 0u, 0u, (uint64_t)e << 32};
+        const uint64_t eh = (uint64_t)e << 32;
+        unsigned long long hs = 0;
+        uint32_t n_direct = 0, n_prot = 0;  // victims handled outside the list; protected victims
         if (belady) {
-          const uint32_t nd_ = hb_total(dead, sm);
-          auto emit_dead = [&](uint32_t lid) { vc(lid); };
-          auto emit_pend = [&](uint32_t q) { vc(nd.lidf[q] & LID_MASK); };
+          // in-flight blocks left `pend` in R2 (their next use is this epoch)
+          const uint32_t nd_ = sm.tot_dead, np_ = sm.tot_pend - inAS;
           if (k <= nd_) {
-            hb_take_top(dead, k, emit_dead, sm);
+            hb_take_top(dead, k, vlist, VT_LID, sm);
           } else {
-            if (nd_ > 0) hb_take_all(dead, emit_dead);
-            const uint32_t np_ = hb_total(pend, sm);
-            if (k - nd_ <= np_) hb_take_top(pend, k - nd_, emit_pend, sm);
-            else if (threadIdx.x == 0) bad = 1;
+            if (nd_ > 0) hb_take_from(dead, 0, 0, 0, vlist, &sm.n_vict, VT_LID);
+            if (k - nd_ <= np_) { __syncthreads(); hb_take_top(pend, k - nd_, vlist, 0u, sm); }
+            else bad = 1;
+          }
+          if (threadIdx.x == 0) {
+            sm.tot_dead = nd_ - min(k, nd_);
+            sm.tot_pend = np_ - (k > nd_ ? k - nd_ : 0u);
           }
         } else {
           const uint32_t* L = lists[cur];
-          // unit eviction: all resident latest positions of unit u (warp-cooperative)
+          // whole-unit eviction: list every resident latest position of unit u (warp-collective)
           auto evict_unit = [&](uint32_t u, bool prot) {
             const uint32_t pa = nd.u_pos[u], pe = nd.u_pos[u + 1];
+            const uint32_t wlast = (pe - 1) >> 5;
             uint32_t taken = 0;
-            for (uint32_t wi = (pa >> 5) + lane; wi <= ((pe - 1) >> 5); wi += 32) {
-              uint32_t m = 0xffffffffu;
-              if (wi == (pa >> 5)) m &= ~((1u << (pa & 31)) - 1u);
-              if (wi == ((pe - 1) >> 5) && (pe & 31)) m &= (1u << (pe & 31)) - 1u;
-              const uint32_t wv = alive[wi] & m;
-              if (wv) {
-                atomicAnd(&alive[wi], ~wv);
-                for (uint32_t x = wv; x; x &= x - 1) vc(nd.lidf[wi * 32u + (uint32_t)(__ffs(x) - 1)] & LID_MASK);
-                taken += __popc(wv);
+            for (uint32_t wb = pa >> 5; wb <= wlast; wb += 32) {
+              const uint32_t wi = wb + lane;
+              uint32_t wv = 0;
+              if (wi <= wlast) {
+                uint32_t m = 0xffffffffu;
+                if (wi == (pa >> 5)) m &= ~((1u << (pa & 31)) - 1u);
+                if (wi == wlast && (pe & 31)) m &= (1u << (pe & 31)) - 1u;
+                wv = alive[wi] & m;
+                if (wv) atomicAnd(&alive[wi], ~wv);
               }
+              emit_bits(vlist, &sm.n_vict, wi, wv, 0u);
+              taken += __popc(wv);
             }
-            if (prot) vc.np += taken;
             taken = warp_sum(taken);
-            if (lane == 0) cnt[u] -= taken;
+            if (lane == 0) { cnt[u] -= taken; if (prot) n_prot += taken; }
           };
           if (!aeg) {  // EVICT_ALL: every candidate
             for (uint32_t i = wid; i < nL; i += RW) {
               const uint32_t u = L[i];
               if (cnt[u]) evict_unit(u, false);
             }
-            __syncthreads();
           } else {
             // pass a: normalisers over cand (eq:recency tau_max, eq:size size_max)
             long long tau = 0;
@@ -486,8 +560,8 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
               tau = max(tau, (long long)(Te - nd.u_t[u]));
               smax = max(smax, owner_size(v, sstate, nd.u_own[u]));
             }
-            tau = block_reduce<RT, long long>(tau, Max(), sm.b.i64);
-            smax = block_reduce<RT, uint32_t>(smax, Max(), sm.b.u32);
+            tau = block_reduce<RT, long long>(tau, Max(), sm.b, par);
+            smax = block_reduce<RT, uint32_t>(smax, Max(), sm.b, par);
             KeyCtx x;
             x.Te = Te; x.tau = tau; x.smax = smax;
             x.den = (int64_t)(a.p_high - a.p_low) * C;
@@ -511,7 +585,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             }
             __syncthreads();
             uint32_t d1, r1, d2, r2;
-            find_level(sm.hist, 0, H1, k, d1, r1, sm);
+            find_level<H1 / RT>(sm.hist, 0, H1, k, d1, r1, sm, par);
             for (uint32_t i = threadIdx.x; i < 1024; i += RT) sm.hist[i] = 0;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
@@ -521,7 +595,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
               if (c) atomicAdd(&sm.hist[kp & 1023u], c);
             }
             __syncthreads();
-            find_level(sm.hist, 0, 1024, r1, d2, r2, sm);
+            find_level<1024 / RT>(sm.hist, 0, 1024, r1, d2, r2, sm, par);
             const uint32_t kps = ((d1 >> 11) << 31) | ((d1 & 2047u) << 10) | d2;
             const bool prot_piv = !(kps >> 31);
             const bool whole = sm.hist[d2] == r2;  // the pivot units are evicted whole
@@ -554,62 +628,89 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
                 uint32_t b0 = 0;
                 if (lane == 31 && tot) b0 = atomicAdd(&sm.n_piv, tot);
                 b0 = __shfl_sync(0xffffffffu, b0, 31) + xs - c;
-                for (uint32_t y = wv; y; y &= y - 1) {
-                  const uint32_t p = wi * 32u + (uint32_t)(__ffs(y) - 1);
-                  kbuf[b0++] = ((uint64_t)(nd.lidf[p] & LID_MASK) << 32) | p;
-                }
+                for (uint32_t y = wv; y; y &= y - 1) kbuf[b0++] = wi * 32u + (uint32_t)(__ffs(y) - 1);
               }
             }
             __syncthreads();
             const uint32_t npv = sm.n_piv;
             if (!whole && npv) {
-              const uint64_t T = radix_select<RT>(kbuf, npv, r2, sm.b);
+              // pivot keys differ only in lid: rank (lid << 32 | position) and keep the top r2
+              for (uint32_t i = threadIdx.x; i < npv; i += RT) {
+                const uint32_t p = (uint32_t)kbuf[i];
+                kbuf[i] = ((uint64_t)(nd.lidf[p] & LID_MASK) << 32) | p;
+              }
+              __syncthreads();
+              const uint64_t T = radix_select<RT>(kbuf, npv, r2, sm.b, par);
               uint32_t tk = 0;
               for (uint32_t i = threadIdx.x; i < npv; i += RT) {
                 const uint64_t kv = kbuf[i];
                 if (kv < T) continue;
-                const uint32_t p = (uint32_t)kv;
+                const uint32_t p = (uint32_t)kv, lid = (uint32_t)(kv >> 32);
                 atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
                 atomicSub(&cnt[nd.u_of[p] & UMASK], 1u);
-                vc((uint32_t)(kv >> 32));
+                res_pos[lid] = NONE;
+                hs += splitmix64(eh | lid);
                 ++tk;
               }
-              if (prot_piv) vc.np += tk;
+              n_direct += tk;
+              if (prot_piv) n_prot += tk;
             }
-            __syncthreads();
           }
         }
-        const uint32_t nv = block_reduce<RT, uint32_t>(vc.n, Add(), sm.b.u32);
-        const uint32_t np = block_reduce<RT, uint32_t>(vc.np, Add(), sm.b.u32);
-        hash += vc.hash;
+        __syncthreads();
+        // listed victims: positions (block at that position) or local ids (VT_LID)
+        const uint32_t nvl = sm.n_vict;
+        for (uint32_t i = threadIdx.x; i < nvl; i += RT) {
+          const uint32_t x = vlist[i];
+          const uint32_t lid = (x & VT_LID) ? (x & ~VT_LID) : (nd.lidf[x] & LID_MASK);
+          res_pos[lid] = NONE;
+          hs += splitmix64(eh | lid);
+        }
+        const unsigned long long nvp = block_reduce<RT, unsigned long long>(
+            ((unsigned long long)n_direct << 32) | n_prot, Add(), sm.b, par);
+        const uint32_t nv = nvl + (uint32_t)(nvp >> 32), np = (uint32_t)nvp;
+        hash += hs;
         if (nv != k) bad = 1;
         S -= nv;
         c_ev += nv; c_prot += aeg ? np : 0; c_evev += 1;  // uniform
       }
       // ---- R4: the last record of each block in the epoch re-enters the index ----
       __syncthreads();
-      if (threadIdx.x == 0) sm.n_app = 0;
-      for (uint64_t wb = (P0 & ~31ull) + (uint64_t)wid * 32u; wb < P1; wb += RT) {
-        const uint64_t pb = wb + lane;
-        const bool in = pb >= P0 && pb < P1;
-        uint32_t q = 0, lid = 0;
-        bool last = false;
-        if (in) {
-          q = nd.nxt[pb];
-          last = (uint64_t)q >= P1;  // INF included
-          if (last) { lid = nd.lidf[pb] & LID_MASK; res_pos[lid] = (uint32_t)pb; }
+      if (threadIdx.x == 0) {
+        sm.n_app = 0;
+        if (belady && kk <= 0) atomicSub(&sm.tot_pend, inAS);  // (R3 already accounted for it)
+      }
+      for (uint64_t wb = (P0 & ~31ull) + (uint64_t)wid * 32u; wb < P1; wb += (uint64_t)RT * UNR) {
+        uint32_t q[UNR], lf[UNR], uo[UNR];
+        bool last[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint64_t pb = wb + (uint64_t)u * RT + lane;
+          const bool in = pb >= P0 && pb < P1;
+          q[u] = in ? nd.nxt[pb] : 0u;
+          lf[u] = in ? nd.lidf[pb] : 0u;
+          uo[u] = (in && !belady) ? nd.u_of[pb] : 0u;
+          last[u] = in && (uint64_t)q[u] >= P1;  // INF included
         }
-        if (belady) {
-          if (last && q == INF32) hb_set(dead, lid);
-          hb_update_warp(pend, last && q != INF32, q, true);
-        } else {
-          const uint32_t wv = __ballot_sync(0xffffffffu, last);
-          if (lane == 0 && wv) atomicOr(&alive[wb >> 5], wv);
-          const uint32_t u = in ? (nd.u_of[pb] & UMASK) : 0u;
-          const uint32_t lm = __ballot_sync(0xffffffffu, last);
-          if (last) {
-            const uint32_t pr = __match_any_sync(lm, u);
-            if (lane == 31 - __clz(pr)) atomicAdd(&cnt[u], (uint32_t)__popc(pr));
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint64_t pb = wb + (uint64_t)u * RT + lane;
+          const uint32_t lid = lf[u] & LID_MASK;
+          if (last[u]) res_pos[lid] = (uint32_t)pb;
+          if (belady) {
+            if (last[u] && q[u] == INF32) hb_set(dead, lid);
+            hb_update_warp(pend, last[u] && q[u] != INF32, q[u], true);
+            const uint32_t md = __ballot_sync(0xffffffffu, last[u] && q[u] == INF32);
+            const uint32_t mp = __ballot_sync(0xffffffffu, last[u] && q[u] != INF32);
+            if (lane == 0 && (md | mp)) { atomicAdd(&sm.tot_dead, __popc(md)); atomicAdd(&sm.tot_pend, __popc(mp)); }
+          } else {
+            const uint32_t wv = __ballot_sync(0xffffffffu, last[u]);
+            if (lane == 0 && wv) atomicOr(&alive[(wb + (uint64_t)u * RT) >> 5], wv);
+            const uint32_t un = uo[u] & UMASK;
+            if (last[u]) {
+              const uint32_t pr = __match_any_sync(wv, un);
+              if (lane == 31 - __clz(pr)) atomicAdd(&cnt[un], (uint32_t)__popc(pr));
+            }
           }
         }
       }
@@ -674,6 +775,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       out[SAGA_C_INFEASIBLE_EPOCH] = infeasible;
       out[SAGA_C_PEAK_RESIDENT] = c_peak;
       out[SAGA_C_EVENT_EPOCHS] = c_events;
+      if (a.item_cyc) a.item_cyc[it] = (unsigned long long)(clock64() - t_start);
     }
     __syncthreads();
   }
@@ -751,9 +853,9 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   uint32_t* hpos = nullptr;
   uint32_t* u_kind = nullptr;
   uint32_t* dmax = nullptr;
-  SAGA_CK(cudaMallocAsync((void**)&head, (N + 1) * 4, s));
-  SAGA_CK(cudaMallocAsync((void**)&hpos, (N + 2) * 4, s));
-  SAGA_CK(cudaMallocAsync((void**)&dmax, 4, s));
+  SAGA_CK(ws_malloc((void**)&head, (N + 1) * 4, s));
+  SAGA_CK(ws_malloc((void**)&hpos, (N + 2) * 4, s));
+  SAGA_CK(ws_malloc((void**)&dmax, 4, s));
   SAGA_CK(cudaMemsetAsync(dmax, 0, 4, s));
   nd.ev_pos = dalloc<uint64_t>(t, size_t(J) + 1);
   nd.u_of = dalloc<uint32_t>(t, N);
@@ -776,7 +878,7 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   nd.u_own = dalloc<uint32_t>(t, nu);
   nd.ev_unit = dalloc<uint32_t>(t, size_t(J) + 1);
   nd.ev_upd = dalloc<uint32_t>(t, J);
-  SAGA_CK(cudaMallocAsync((void**)&u_kind, (size_t(nu) + 1) * 4, s));
+  SAGA_CK(ws_malloc((void**)&u_kind, (size_t(nu) + 1) * 4, s));
   if (!nd.u_pos || !nd.u_t || !nd.u_own || !nd.ev_unit || !nd.ev_upd) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
   if (N > 0) {
     k_unit_fill<<<grid_for(N), NTHREADS, 0, s>>>(head, hpos, N, nd.lidf, nd.lown, nd.g_pos, nd.G, nd.g_t, nd.g_kind,
@@ -792,10 +894,10 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   SAGA_CK_LAUNCH();
   SAGA_CK(cudaStreamSynchronize(s));
   nd.max_ev_units = hm;
-  cudaFreeAsync(head, s);
-  cudaFreeAsync(hpos, s);
-  cudaFreeAsync(u_kind, s);
-  cudaFreeAsync(dmax, s);
+  ws_free(head, s);
+  ws_free(hpos, s);
+  ws_free(u_kind, s);
+  ws_free(dmax, s);
   nd.rp_done = true;
   return SAGA_OK;
 }
@@ -840,7 +942,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
     for (uint32_t pi = 0; pi < n_pol; ++pi)
       for (uint32_t ni = 0; ni < n_owned; ++ni) items.push_back((pi << 28) | (ci << 12) | ni);
   const uint32_t n_items = (uint32_t)items.size();
-  // per-CTA scratch layout (all offsets 16-byte aligned)
+  // per-CTA scratch layout (all offsets 256-byte aligned)
   auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
   const uint64_t n2N = std::max<uint64_t>(1, (maxN + (1u << 20) - 1) >> 20);
   const uint64_t n2L = std::max<uint64_t>(1, (max_local + (1u << 20) - 1) >> 20);
@@ -849,36 +951,49 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   a.o_res = off; off += al(max_local * 4 + 16);
   a.o_bits = off; off += al(n2N * 32768 * 4);
   a.o_c1 = off; off += al(n2N * 1024 * 4);
-  a.o_c2 = off; off += al(n2N * 4);
   a.o_dbits = off; off += al(n2L * 32768 * 4);
   a.o_dc1 = off; off += al(n2L * 1024 * 4);
-  a.o_dc2 = off; off += al(n2L * 4);
   a.o_cnt = off; off += al(max_units * 4);
   a.o_list0 = off; off += al(max_units * 4);
   a.o_list1 = off; off += al(max_units * 4);
   a.o_lkp = off; off += al(max_units * 4);
   a.o_kbuf = off; off += al(((uint64_t)cap_max + 1) * 8);
+  a.o_vl = off; off += al(((uint64_t)cap_max + 1) * 4);
   a.o_sst = off; off += al((uint64_t)std::max(v.n_sessions, 1u) * 4);
   a.cta_bytes = off;
+  // dynamic shared memory: the c2 counts always; the c1 counts (BELADY) and the unit counts
+  // (AEG / EVICT_ALL; same region) when they fit
+  const uint64_t dyn_max = 160ull * 1024;
+  const uint64_t c2_bytes = ((n2N + n2L + 3) & ~3ull) * 4;
+  const uint64_t c1_bytes = (n2N + n2L) * 1024 * 4;
+  a.n2N_max = (uint32_t)n2N; a.n2L_max = (uint32_t)n2L;
+  a.dyn_c1 = (c2_bytes + c1_bytes <= dyn_max) ? 1u : 0u;
+  uint64_t dyn = std::max<uint64_t>(a.dyn_c1 ? c2_bytes + c1_bytes : c2_bytes, std::min<uint64_t>(max_units * 4, dyn_max));
+  dyn = (dyn + 15) & ~15ull;
+  a.dyn_words = (uint32_t)(dyn / 4);
+  SAGA_CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_replay, RT, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_replay, RT, (size_t)dyn);
   uint32_t grid = std::min<uint32_t>(n_items, (uint32_t)nsm * (uint32_t)std::max(occ, 1));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   const uint64_t budget = free_b > (4ull << 30) ? (free_b - (4ull << 30)) / 2 : free_b / 4;
   grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(grid, budget / std::max<uint64_t>(a.cta_bytes, 1)));
+  const bool trace = getenv("SAGA_REPLAY_TRACE") != nullptr;
   NodeArr* d_nodes = nullptr;
   uint32_t *d_caps = nullptr, *d_list = nullptr, *d_items = nullptr, *work = nullptr;
+  unsigned long long* d_cyc = nullptr;
   uint8_t* scratch = nullptr;
-  SAGA_CK(cudaMallocAsync((void**)&d_nodes, sizeof(NodeArr) * t->n_nodes, s));
-  SAGA_CK(cudaMallocAsync((void**)&d_caps, 4 * n_caps, s));
-  SAGA_CK(cudaMallocAsync((void**)&d_list, 4 * n_owned, s));
-  SAGA_CK(cudaMallocAsync((void**)&d_items, 4 * n_items, s));
-  SAGA_CK(cudaMallocAsync((void**)&work, 8, s));
-  if (cudaMallocAsync((void**)&scratch, a.cta_bytes * grid, s) != cudaSuccess) {
+  SAGA_CK(ws_malloc((void**)&d_nodes, sizeof(NodeArr) * t->n_nodes, s));
+  SAGA_CK(ws_malloc((void**)&d_caps, 4 * n_caps, s));
+  SAGA_CK(ws_malloc((void**)&d_list, 4 * n_owned, s));
+  SAGA_CK(ws_malloc((void**)&d_items, 4 * n_items, s));
+  SAGA_CK(ws_malloc((void**)&work, 8, s));
+  if (trace) SAGA_CK(ws_malloc((void**)&d_cyc, 8ull * n_items, s));
+  if (ws_malloc((void**)&scratch, a.cta_bytes * grid, s) != cudaSuccess) {
     set_error("out of device memory (replay scratch %llu bytes)", (unsigned long long)(a.cta_bytes * grid));
     return SAGA_ERR_OOM;
   }
@@ -893,18 +1008,31 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   a.n_caps = n_caps; a.n_nodes_total = t->n_nodes; a.counters = counters;
   a.alpha = cfg->alpha; a.beta = cfg->beta; a.gamma = cfg->gamma;
   a.p_low = cfg->p_low_pm; a.p_high = cfg->p_high_pm; a.ttl_max = cfg->ttl_max_us;
-  a.scratch = scratch; a.work = work; a.err = work + 1;
+  a.scratch = scratch; a.work = work; a.err = work + 1; a.item_cyc = d_cyc;
   prof_begin(SAGA_PROF_REPLAY, s);
-  k_replay<<<grid, RT, 0, s>>>(a);
+  k_replay<<<grid, RT, dyn, s>>>(a);
   prof_end(SAGA_PROF_REPLAY, s);
   count_launch();
   SAGA_CK_LAUNCH();
   uint32_t herr = 0;
   SAGA_CK(cudaMemcpyAsync(&herr, work + 1, 4, cudaMemcpyDeviceToHost, s));
-  cudaFreeAsync(d_nodes, s); cudaFreeAsync(d_caps, s); cudaFreeAsync(d_list, s); cudaFreeAsync(d_items, s);
-  cudaFreeAsync(scratch, s);
-  cudaFreeAsync(work, s);
+  std::vector<unsigned long long> cyc(trace ? n_items : 0);
+  if (trace) SAGA_CK(cudaMemcpyAsync(cyc.data(), d_cyc, 8ull * n_items, cudaMemcpyDeviceToHost, s));
+  ws_free(d_nodes, s); ws_free(d_caps, s); ws_free(d_list, s); ws_free(d_items, s);
+  ws_free(scratch, s);
+  ws_free(work, s);
+  if (d_cyc) ws_free(d_cyc, s);
   SAGA_CK(cudaStreamSynchronize(s));
+  if (trace) {
+    fprintf(stderr, "[saga replay] grid %u x %d threads, dyn smem %llu B (c1 %s), %u items\n", grid, RT,
+            (unsigned long long)dyn, a.dyn_c1 ? "smem" : "global", n_items);
+    for (uint32_t i = 0; i < n_items; ++i) {
+      const uint32_t pk = items[i];
+      const uint32_t w = nodes[pk & 0xFFFu];
+      fprintf(stderr, "[saga replay] item pol=%u cap=%u node=%u events=%u Mcycles=%.2f\n", pol[pk >> 28],
+              caps[(pk >> 12) & 0xFFFFu], w, t->nodes[w].J, cyc[i] / 1e6);
+    }
+  }
   if (herr) { set_error("saga_replay: internal selection check failed"); return SAGA_ERR_STATE; }
   return SAGA_OK;
 }

@@ -63,6 +63,7 @@ __device__ __forceinline__ OwnerKeyIn owner_at(const TraceView& v, uint32_t o, u
 
 __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
   __shared__ BlockScratch<ST> sm;
+  Par par;
   const TraceView& v = a.v;
   for (uint32_t sg = blockIdx.x; sg < a.b.n_seg; sg += gridDim.x) {
     const uint64_t c0 = a.b.seg_off[sg], c1 = a.b.seg_off[sg + 1];
@@ -90,8 +91,8 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
       }
       smax = max(smax, last_sz);
     }
-    tau = block_reduce<ST, long long>(tau, Max(), sm.i64);
-    smax = block_reduce<ST, uint32_t>(smax, Max(), sm.u32);
+    tau = block_reduce<ST, long long>(tau, Max(), sm, par);
+    smax = block_reduce<ST, uint32_t>(smax, Max(), sm, par);
     KeyCtx x;
     x.Te = Te; x.tau = tau; x.smax = smax;
     x.den = (int64_t)(a.p_high - a.p_low) * C;
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(SLT) k_select(const uint64_t* __restrict__ key
                                                 uint64_t* scratch_k, uint32_t* scratch_i, uint64_t scratch_per_cta) {
   __shared__ BlockScratch<SLT> sm;
   __shared__ uint32_t s_cnt;
+  Par par;
   uint64_t* sk = scratch_k + (uint64_t)blockIdx.x * scratch_per_cta;
   uint32_t* si = scratch_i + (uint64_t)blockIdx.x * scratch_per_cta;
   for (uint32_t sg = blockIdx.x; sg < n_seg; sg += gridDim.x) {
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(SLT) k_select(const uint64_t* __restrict__ key
     if (k > n) k = n;
     if (k == 0) continue;
     const uint64_t* kb = key + c0;
-    const uint64_t T = (k < n) ? radix_select<SLT>(kb, n, k, sm) : 0ull;
+    const uint64_t T = (k < n) ? radix_select<SLT>(kb, n, k, sm, par) : 0ull;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     uint32_t np2 = 1;
@@ -192,7 +194,7 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
   std::vector<ScoreNode> hn(t->n_nodes);
   for (uint32_t w = 0; w < t->n_nodes; ++w) { hn[w].lown = t->nodes[w].lown; hn[w].n_local = t->nodes[w].n_local; }
   ScoreNode* dn = nullptr;
-  SAGA_CK(cudaMallocAsync((void**)&dn, sizeof(ScoreNode) * t->n_nodes, s));
+  SAGA_CK(ws_malloc((void**)&dn, sizeof(ScoreNode) * t->n_nodes, s));
   SAGA_CK(cudaMemcpyAsync(dn, hn.data(), sizeof(ScoreNode) * t->n_nodes, cudaMemcpyHostToDevice, s));
   ScoreArgs a{};
   a.v = t->v; a.nodes = dn; a.b = *b;
@@ -205,7 +207,7 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
   prof_end(SAGA_PROF_SCORE, s);
   count_launch();
   SAGA_CK_LAUNCH();
-  cudaFreeAsync(dn, s);
+  ws_free(dn, s);
   return SAGA_OK;
 }
 
@@ -223,15 +225,15 @@ saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint3
   const unsigned grid = std::min<unsigned>(n_seg, nsm_count());
   uint64_t* sk = nullptr;
   uint32_t* si = nullptr;
-  SAGA_CK(cudaMallocAsync((void**)&sk, 8 * np2 * grid, s));
-  SAGA_CK(cudaMallocAsync((void**)&si, 4 * np2 * grid, s));
+  SAGA_CK(ws_malloc((void**)&sk, 8 * np2 * grid, s));
+  SAGA_CK(ws_malloc((void**)&si, 4 * np2 * grid, s));
   prof_begin(SAGA_PROF_SELECT, s);
   k_select<<<grid, SLT, 0, s>>>(key, seg_off, k, n_seg, out_off, victim, sk, si, np2);
   prof_end(SAGA_PROF_SELECT, s);
   count_launch();
   SAGA_CK_LAUNCH();
-  cudaFreeAsync(sk, s);
-  cudaFreeAsync(si, s);
+  ws_free(sk, s);
+  ws_free(si, s);
   return SAGA_OK;
 }
 

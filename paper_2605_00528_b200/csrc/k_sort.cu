@@ -215,11 +215,11 @@ cudaError_t onesweep_sort_pairs(saga_trace* t, const uint32_t* keys_in, uint64_t
   uint32_t *kA = nullptr, *vA = nullptr, *hist = nullptr, *status = nullptr, *tctr = nullptr;
   cudaError_t e;
   // ping-pong buffers: pass p writes (p odd -> out) so that the last pass lands in *_out
-  if ((e = cudaMallocAsync((void**)&kA, n * 4, s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync((void**)&vA, n * 4, s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync((void**)&hist, MAXPASS * RADIX * 4, s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync((void**)&status, tiles * RADIX * 4 * npass, s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync((void**)&tctr, 4 * MAXPASS, s)) != cudaSuccess) return e;
+  if ((e = ws_malloc((void**)&kA, n * 4, s)) != cudaSuccess) return e;
+  if ((e = ws_malloc((void**)&vA, n * 4, s)) != cudaSuccess) return e;
+  if ((e = ws_malloc((void**)&hist, MAXPASS * RADIX * 4, s)) != cudaSuccess) return e;
+  if ((e = ws_malloc((void**)&status, tiles * RADIX * 4 * npass, s)) != cudaSuccess) return e;
+  if ((e = ws_malloc((void**)&tctr, 4 * MAXPASS, s)) != cudaSuccess) return e;
   cudaMemsetAsync(hist, 0, MAXPASS * RADIX * 4, s);
   cudaMemsetAsync(status, 0, tiles * RADIX * 4 * npass, s);
   cudaMemsetAsync(tctr, 0, 4 * MAXPASS, s);
@@ -251,11 +251,11 @@ cudaError_t onesweep_sort_pairs(saga_trace* t, const uint32_t* keys_in, uint64_t
     vi = vo;
   }
   e = cudaGetLastError();
-  cudaFreeAsync(kA, s);
-  cudaFreeAsync(vA, s);
-  cudaFreeAsync(hist, s);
-  cudaFreeAsync(status, s);
-  cudaFreeAsync(tctr, s);
+  ws_free(kA, s);
+  ws_free(vA, s);
+  ws_free(hist, s);
+  ws_free(status, s);
+  ws_free(tctr, s);
   return e;
 }
 

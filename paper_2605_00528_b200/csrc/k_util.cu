@@ -91,7 +91,7 @@ template <class T>
 cudaError_t scan_impl(saga_trace* t, const T* in, T* out, uint64_t n) {
   uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   T* sums = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&sums, (nb + 1) * sizeof(T), t->stream);
+  cudaError_t e = ws_malloc((void**)&sums, (nb + 1) * sizeof(T), t->stream);
   if (e != cudaSuccess) return e;
   if (nb > 0) {
     k_tile_reduce<T><<<(unsigned)nb, SCAN_T, 0, t->stream>>>(in, n, sums);
@@ -104,7 +104,7 @@ cudaError_t scan_impl(saga_trace* t, const T* in, T* out, uint64_t n) {
     count_launch();
   }
   e = cudaGetLastError();
-  cudaFreeAsync(sums, t->stream);
+  ws_free(sums, t->stream);
   return e;
 }
 }  // namespace

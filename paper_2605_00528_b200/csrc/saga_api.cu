@@ -58,6 +58,62 @@ void prof_end(int cat, cudaStream_t s) {
   }
 }
 
+// ---------------- workspace cache ----------------
+namespace ws_detail {
+struct Blk { void* p; size_t size; int dev; cudaStream_t s; bool used; };
+std::mutex g_ws_mu;
+std::vector<Blk> g_ws;
+}  // namespace ws_detail
+
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s) {
+  using namespace ws_detail;
+  if (bytes == 0) bytes = 1;
+  const size_t gran = bytes <= (1ull << 20) ? 512 : (1ull << 20);
+  const size_t want = (bytes + gran - 1) & ~(gran - 1);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    size_t best = SIZE_MAX, bi = 0;
+    for (size_t i = 0; i < g_ws.size(); ++i) {
+      const Blk& b = g_ws[i];
+      if (b.used || b.dev != dev || b.s != s || b.size < want || b.size > 2 * want + gran) continue;
+      if (b.size < best) { best = b.size; bi = i; }
+    }
+    if (best != SIZE_MAX) { g_ws[bi].used = true; *p = g_ws[bi].p; return cudaSuccess; }
+  }
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, want);
+  if (e != cudaSuccess) {  // release cached idle blocks of this device and retry once
+    cudaGetLastError();
+    std::vector<void*> drop;
+    {
+      std::lock_guard<std::mutex> g(g_ws_mu);
+      for (size_t i = 0; i < g_ws.size();) {
+        if (!g_ws[i].used && g_ws[i].dev == dev) { drop.push_back(g_ws[i].p); g_ws.erase(g_ws.begin() + (long)i); }
+        else ++i;
+      }
+    }
+    cudaDeviceSynchronize();
+    for (void* x : drop) cudaFree(x);
+    e = cudaMalloc(&q, want);
+    if (e != cudaSuccess) return e;
+  }
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  g_ws.push_back({q, want, dev, s, true});
+  *p = q;
+  return cudaSuccess;
+}
+
+// stream-ordered release: later work on the same stream may reuse the block
+void ws_free(void* p, cudaStream_t s) {
+  using namespace ws_detail;
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  for (Blk& b : g_ws)
+    if (b.p == p) { b.used = false; b.s = s; return; }
+}
+
 static void mempool_setup(int device) {
   static std::mutex mu;
   static uint64_t done_mask = 0;
@@ -125,7 +181,7 @@ void saga_free_trace(saga_trace* t) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(t->device);
-  for (void* p : t->allocs) cudaFreeAsync(p, t->stream);
+  for (void* p : t->allocs) ws_free(p, t->stream);
   cudaStreamSynchronize(t->stream);
   cudaSetDevice(prev);
   delete t;

@@ -26,6 +26,11 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 
 void set_error(const char* fmt, ...);
 
+// Stream-ordered workspace cache (saga_api.cu): blocks are cudaMalloc'ed once and recycled per
+// (device, stream), so the hot path never grows a memory pool inside a timed step.
+cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s);
+void ws_free(void* p, cudaStream_t s);
+
 // device-time profile (saga_profile_enable / saga_profile_read)
 void prof_begin(int cat, cudaStream_t s);
 void prof_end(int cat, cudaStream_t s);
@@ -147,7 +152,7 @@ template <class T>
 T* dalloc(saga_trace* t, size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
-  if (cudaMallocAsync(&p, n * sizeof(T), t->stream) != cudaSuccess) return nullptr;
+  if (ws_malloc(&p, n * sizeof(T), t->stream) != cudaSuccess) return nullptr;
   t->allocs.push_back(p);
   return static_cast<T*>(p);
 }
