@@ -51,9 +51,32 @@ struct HB {
   uint32_t n2;
 };
 
+constexpr uint32_t LO_SHARED = 0x80000000u;  // local owner tag: shared prefix of type (lo & ~LO_SHARED)
+
+// static description of a unit (maximal run of one record group with one owner)
+struct __align__(8) UnitRec {
+  int64_t t;        // t_last of its blocks: t_c of the CALL group, T_e of a MIG group
+  uint32_t pa, pe;  // positions [pa, pe)
+  uint32_t lo;      // local owner id (private session) or LO_SHARED | type
+  uint32_t pad;
+};
+// live-list entry: the unit record plus the per-event key part
+struct __align__(16) ListRec {
+  int64_t t;
+  uint32_t u, pa, pe, lo, kp, pad;
+};
+// per-call inputs of the WA-LRU key of a private session whose newest call is c
+struct __align__(8) CallKey {
+  int64_t tend;     // tool start (Alg. 1 elapsed-time origin)
+  float P;          // P_reuse (eq:reuse with eq:overlap), fp32 pinned
+  uint32_t size;    // ceil(n_cur / block_tokens) (eq:size numerator)
+  uint32_t ttl;     // ttl_base of the call's AEG node (<= 1e9)
+  uint32_t fin;     // is_last || terminal
+};
+
 struct NodeArr {
   uint64_t N;
-  uint32_t J, n_local, n_units, pad;
+  uint32_t J, n_local, n_units, n_lo;
   const uint64_t* ev_pos;
   const uint32_t* ev_e;
   const uint32_t* ev_inv;
@@ -64,11 +87,10 @@ struct NodeArr {
   const uint32_t* lidf;
   const uint32_t* nxt;
   const uint32_t* u_of;
-  const uint32_t* u_pos;
-  const int64_t* u_t;
-  const uint32_t* u_own;
+  const UnitRec* urec;
   const uint32_t* lid2gid;
   const uint32_t* upd_c;
+  const uint32_t* upd_lo;
 };
 
 struct ReplayArgs {
@@ -88,13 +110,18 @@ struct ReplayArgs {
   // per-CTA scratch (strides in elements)
   uint8_t* scratch;
   uint64_t cta_bytes;
-  uint64_t o_res, o_bits, o_c1, o_dbits, o_dc1, o_cnt, o_list0, o_list1, o_lkp, o_kbuf, o_vl, o_sst;
+  const CallKey* callkey;
+  uint64_t o_res, o_runit, o_bits, o_c1, o_dbits, o_dc1, o_cnt, o_list0, o_list1, o_kbuf, o_vl, o_ocall;
   uint32_t n2N_max, n2L_max;   // c2 entries of the two bitmaps (dynamic shared memory)
-  uint32_t dyn_c1;             // the c1 arrays are in dynamic shared memory too
+  uint32_t dyn_c1;             // BELADY: the c1 arrays are in dynamic shared memory too
+  uint32_t dyn_dbits_words;    // BELADY: dead bits in shared memory when n_local <= 32 * this
   uint32_t dyn_words;          // dynamic shared memory size in 32-bit words
+  uint32_t ocall_smem;         // AEG: newest-call table (n_lo words) in shared memory
   unsigned long long* item_cyc;  // optional per-item SM cycles (SAGA_REPLAY_TRACE)
+  unsigned long long* phase_cyc; // optional [item][8] per-phase cycles of thread 0
   uint32_t* work;
   uint32_t* err;
+  uint32_t* dbg;  // [4] first failed invariant
 };
 
 struct Smem {
@@ -106,6 +133,11 @@ struct Smem {
   uint32_t ilo, ihi;
   uint32_t tot_dead, tot_pend;  // BELADY: set bits of the two hierarchical bitmaps
 };
+
+// first failed invariant of the launch: [0] = line, [1..3] = values (host reports it)
+__device__ __forceinline__ void dbg_fail(uint32_t* dbg, uint32_t line, uint32_t x, uint32_t y, uint32_t z) {
+  if (atomicCAS(&dbg[0], 0u, line) == 0u) { dbg[1] = x; dbg[2] = y; dbg[3] = z; }
+}
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
 #pragma unroll
@@ -223,11 +255,12 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
 
 // take the k highest set bits (1 <= k <= total).  The threshold is found by warp 0 alone
 // (c2 level, then the 1024 c1 entries of the pivot c2 block as 32 lanes x 32, then 32 words).
-__device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t tag, Smem& sm) {
+__device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t tag, Smem& sm, uint32_t* dbg) {
   if (threadIdx.x < 32) {
     const uint32_t lane = threadIdx.x;
+    if (lane == 0) sm.thr = NONE;
     // c2 level
-    uint32_t carry = 0, j2 = 0, r2 = 0;
+    uint32_t carry = 0, j2 = NONE, r2 = 0;
     for (uint32_t base = 0; base < h.n2; base += 32) {
       const uint32_t idx = h.n2 - 1 - (base + lane);
       const uint32_t v = base + lane < h.n2 ? h.c2[idx] : 0u;
@@ -246,6 +279,8 @@ __device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t t
       }
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
+    if (j2 == NONE) { if (lane == 0) dbg_fail(dbg, __LINE__, k, carry, h.n2); goto done; }
+    {
     // c1 level: lane l owns entries [top - 32 l - 31, top - 32 l] of block j2
     const uint32_t b0 = j2 * 1024u + 1024u - 32u * (lane + 1);
     const uint4* c4 = reinterpret_cast<const uint4*>(h.c1 + b0);
@@ -264,6 +299,7 @@ __device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t t
       if (lane >= (uint32_t)o) x += y;
     }
     const uint32_t hit = __ballot_sync(0xffffffffu, x - sum < r2 && r2 <= x);
+    if (!hit) { if (lane == 0) dbg_fail(dbg, __LINE__, k, r2, j2); goto done; }
     const int L = __ffs(hit) - 1;
     uint32_t j1 = 0, r1 = 0;
     if ((int)lane == L) {
@@ -294,9 +330,12 @@ __device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t t
       sm.hb_j2 = j2;
       sm.hb_j1 = j1;
     }
+    if (!__ballot_sync(0xffffffffu, xw - cw < r1 && r1 <= xw) && lane == 0) dbg_fail(dbg, __LINE__, k, r1, j1);
+    }
+  done:;
   }
   __syncthreads();
-  hb_take_from(h, sm.hb_j2, sm.hb_j1, sm.thr, vlist, &sm.n_vict, tag);
+  if (sm.thr != NONE) hb_take_from(h, sm.hb_j2, sm.hb_j1, sm.thr, vlist, &sm.n_vict, tag);
 }
 
 __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
@@ -305,51 +344,66 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
   return lo;
 }
 
-// owner state of a private session / shared prefix at the current boundary
-__device__ __forceinline__ OwnerKeyIn owner_in(const TraceView& v, const uint32_t* sstate, uint32_t o, uint32_t act) {
+// owner inputs of the WA-LRU key at the current boundary (lo = local owner id or shared type)
+__device__ __forceinline__ OwnerKeyIn owner_in(const TraceView& v, const CallKey* ck, const uint32_t* ocall, uint32_t lo,
+                                               uint32_t act) {
   OwnerKeyIn r;
-  if (o >= v.n_sessions) {
-    const uint32_t t = o - v.n_sessions;
+  if (lo & LO_SHARED) {
+    const uint32_t t = lo & ~LO_SHARED;
     const bool on = (act >> t) & 1u;
-    r.shared = true; r.prot_shared = on; r.size = v.tlen[t]; r.P = on ? 1.0f : 0.0f;
+    r.shared = true; r.prot_shared = on; r.size = __ldg(&v.tlen[t]); r.P = on ? 1.0f : 0.0f;
     r.fin = false; r.t_call = 0; r.ttl_base = 0;
     return r;
   }
-  const uint32_t c1 = sstate[o];
-  const uint32_t c = c1 ? c1 - 1 : 0;
+  const uint32_t c1 = ocall[lo];
+  const CallKey k = ck[c1 ? c1 - 1 : 0];
   r.shared = false; r.prot_shared = false;
-  r.size = __ldg(&v.ci_size[c]);
-  r.fin = __ldg(&v.ci_fin[c]) != 0;
-  r.P = __ldg(&v.ci_P[c]);
-  r.t_call = __ldg(&v.tend[c]);
-  r.ttl_base = __ldg(&v.ttl[__ldg(&v.call_v[c])]);
+  r.size = k.size; r.fin = k.fin != 0; r.P = k.P; r.t_call = k.tend; r.ttl_base = (int64_t)k.ttl;
   return r;
 }
 
-__device__ __forceinline__ uint32_t owner_size(const TraceView& v, const uint32_t* sstate, uint32_t o) {
-  if (o >= v.n_sessions) return v.tlen[o - v.n_sessions];
-  const uint32_t c1 = sstate[o];
-  return __ldg(&v.ci_size[c1 ? c1 - 1 : 0]);
+__device__ __forceinline__ uint32_t owner_size(const TraceView& v, const CallKey* ck, const uint32_t* ocall, uint32_t lo) {
+  if (lo & LO_SHARED) return __ldg(&v.tlen[lo & ~LO_SHARED]);
+  const uint32_t c1 = ocall[lo];
+  return ck[c1 ? c1 - 1 : 0].size;
 }
+
+// per-phase SM cycles of thread 0 (SAGA_REPLAY_TRACE): 0 updates+R1, 1 R2, 2 R3 normalisers,
+// 3 R3 keys+pivot, 4 R3 evict, 5 victims, 6 R4, 7 live list
+#define PH(i)                                                   \
+  do {                                                          \
+    if (a.phase_cyc && threadIdx.x == 0) {                      \
+      const long long _n = clock64();                           \
+      ph[i] += _n - ph_t;                                       \
+      ph_t = _n;                                                \
+    }                                                           \
+  } while (0)
 
 constexpr uint32_t VT_LID = 0x80000000u;  // victim-list tag: the entry is a local id, else a position
 constexpr int UNR = 4;                    // record chunks whose loads are issued together (R2 / R4)
 
+__device__ __forceinline__ uint32_t unit_mask(uint32_t wi, uint32_t pa, uint32_t pe) {
+  uint32_t m = 0xffffffffu;
+  if (wi == (pa >> 5)) m &= ~((1u << (pa & 31)) - 1u);
+  if (wi == ((pe - 1) >> 5) && (pe & 31)) m &= (1u << (pe & 31)) - 1u;
+  return m;
+}
+
 __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
   __shared__ Smem sm;
   __shared__ long long s_ctr[SAGA_NCOUNT];
-  extern __shared__ __align__(16) uint32_t dyn[];  // c2 (+ c1) counts / AEG unit counts
+  extern __shared__ __align__(16) uint32_t dyn[];
   Par par;
   const TraceView& v = a.v;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* base = a.scratch + (uint64_t)blockIdx.x * a.cta_bytes;
   uint32_t* res_pos = reinterpret_cast<uint32_t*>(base + a.o_res);
+  uint32_t* res_unit = reinterpret_cast<uint32_t*>(base + a.o_runit);
   uint32_t* alive = reinterpret_cast<uint32_t*>(base + a.o_bits);   // AEG / EVICT_ALL (aliases pend.bits)
-  uint32_t* lists[2] = {reinterpret_cast<uint32_t*>(base + a.o_list0), reinterpret_cast<uint32_t*>(base + a.o_list1)};
-  uint32_t* lkp = reinterpret_cast<uint32_t*>(base + a.o_lkp);
+  ListRec* lists[2] = {reinterpret_cast<ListRec*>(base + a.o_list0), reinterpret_cast<ListRec*>(base + a.o_list1)};
   uint64_t* kbuf = reinterpret_cast<uint64_t*>(base + a.o_kbuf);
   uint32_t* vlist = reinterpret_cast<uint32_t*>(base + a.o_vl);
-  uint32_t* sstate = reinterpret_cast<uint32_t*>(base + a.o_sst);
+  const CallKey* ck = a.callkey;
 
   while (true) {
     if (threadIdx.x == 0) sm.item = atomicAdd(a.work, 1u);
@@ -368,32 +422,38 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
     const bool aeg = pol == SAGA_POLICY_AEG;
     const uint32_t n2N = max(1u, (uint32_t)((nd.N + (1u << 20) - 1) >> 20));
     const uint32_t n2L = max(1u, (nd.n_local + (1u << 20) - 1) >> 20);
-    // count arrays: c2 always in shared memory, c1 there too when it fits (a.dyn_c1)
+    const uint32_t n1L = (nd.n_local + 1023u) >> 10;  // c1 blocks holding local ids
+    // BELADY: c2 always in shared memory; c1 and the dead bits there too when they fit
     uint32_t* c2N = dyn;
     uint32_t* c2L = dyn + a.n2N_max;
-    uint32_t* c1N = a.dyn_c1 ? dyn + ((a.n2N_max + a.n2L_max + 3u) & ~3u) : reinterpret_cast<uint32_t*>(base + a.o_c1);
+    const uint32_t c1off = (a.n2N_max + a.n2L_max + 3u) & ~3u;
+    uint32_t* c1N = a.dyn_c1 ? dyn + c1off : reinterpret_cast<uint32_t*>(base + a.o_c1);
     uint32_t* c1L = a.dyn_c1 ? c1N + a.n2N_max * 1024u : reinterpret_cast<uint32_t*>(base + a.o_dc1);
+    const uint32_t dboff = a.dyn_c1 ? c1off + (a.n2N_max + a.n2L_max) * 1024u : c1off;
+    uint32_t* dbits = (n1L * 32u <= a.dyn_dbits_words) ? dyn + dboff : reinterpret_cast<uint32_t*>(base + a.o_dbits);
     HB pend{reinterpret_cast<uint32_t*>(base + a.o_bits), c1N, c2N, n2N};
-    HB dead{reinterpret_cast<uint32_t*>(base + a.o_dbits), c1L, c2L, n2L};
-    // AEG / EVICT_ALL unit counts: in shared memory when they fit
-    uint32_t* cnt = (a.dyn_words >= nd.n_units) ? dyn : reinterpret_cast<uint32_t*>(base + a.o_cnt);
+    HB dead{dbits, c1L, c2L, n2L};
+    // AEG / EVICT_ALL: newest-call table, then the unit counts, in shared memory when they fit
+    uint32_t* ocall = a.ocall_smem ? dyn : reinterpret_cast<uint32_t*>(base + a.o_ocall);
+    const uint32_t cnt_off = a.ocall_smem ? ((nd.n_lo + 3u) & ~3u) : 0u;
+    uint32_t* cnt = (cnt_off + nd.n_units <= a.dyn_words) ? dyn + cnt_off : reinterpret_cast<uint32_t*>(base + a.o_cnt);
     // ---- reset the item state ----
     {
       const uint4 ones = make_uint4(NONE, NONE, NONE, NONE), zero = make_uint4(0, 0, 0, 0);
       uint4* r4 = reinterpret_cast<uint4*>(res_pos);
       for (uint32_t i = threadIdx.x; i < (nd.n_local + 3) / 4; i += RT) r4[i] = ones;
       uint4* b4 = reinterpret_cast<uint4*>(pend.bits);
-      for (uint32_t i = threadIdx.x; i < n2N * 8192u; i += RT) b4[i] = zero;
+      // whole 1024-bit blocks: the threshold search reads all 32 words of a block
+      for (uint32_t i = threadIdx.x; i < (uint32_t)((nd.N + 1023) / 1024) * 8u; i += RT) b4[i] = zero;
       if (belady) {
         for (uint32_t i = threadIdx.x; i < n2N * 1024u; i += RT) c1N[i] = 0;
         for (uint32_t i = threadIdx.x; i < n2L * 1024u; i += RT) c1L[i] = 0;
         for (uint32_t i = threadIdx.x; i < a.n2N_max + a.n2L_max; i += RT) dyn[i] = 0;
-        uint4* d4 = reinterpret_cast<uint4*>(dead.bits);
-        for (uint32_t i = threadIdx.x; i < n2L * 8192u; i += RT) d4[i] = zero;
+        for (uint32_t i = threadIdx.x; i < n1L * 32u; i += RT) dbits[i] = 0;
       } else {
         for (uint32_t i = threadIdx.x; i < nd.n_units; i += RT) cnt[i] = 0;
+        if (aeg) for (uint32_t i = threadIdx.x; i < nd.n_lo; i += RT) ocall[i] = 0;
       }
-      if (aeg) for (uint32_t i = threadIdx.x; i < v.n_sessions; i += RT) sstate[i] = 0;
       if (threadIdx.x < SAGA_NCOUNT) s_ctr[threadIdx.x] = 0;
       if (threadIdx.x == 0) { sm.tot_dead = 0; sm.tot_pend = 0; }
       __syncthreads();
@@ -406,6 +466,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
     long long c_ev = 0, c_prot = 0, c_evev = 0, c_events = 0, c_peak = 0, infeasible = 0;
     unsigned long long hash = 0;
     uint32_t bad = 0;
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_t = clock64();
 
     for (uint32_t j = 0; j < nd.J; ++j) {
       const uint32_t e = nd.ev_e[j];
@@ -413,10 +474,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       // ---- AEG session state at T_e: newest call c* with e(c*) <= e ----
       if (aeg && j + 1 < nd.J) {
         const uint32_t ue = nd.ev_upd[j];
-        for (uint32_t i = ucur + threadIdx.x; i < ue; i += RT) {
-          const uint32_t c = nd.upd_c[i];
-          atomicMax(&sstate[v.call_sess[c]], c + 1);
-        }
+        for (uint32_t i = ucur + threadIdx.x; i < ue; i += RT) atomicMax(&ocall[nd.upd_lo[i]], nd.upd_c[i] + 1);
         ucur = ue;
       }
       // ---- R1: invalidate the blocks of sessions migrated away ----
@@ -441,7 +499,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             else { hb_clear(pend, q); atomicSub(&sm.tot_pend, 1u); }
           } else {
             atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
-            atomicSub(&cnt[nd.u_of[p] & UMASK], 1u);
+            atomicSub(&cnt[res_unit[l]], 1u);
           }
         }
         nrm = block_reduce<RT, uint32_t>(nrm, Add(), sm.b, par);
@@ -453,11 +511,12 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       if (P0 == P1) continue;    // only empty record groups (the oracle skips the epoch)
       __syncthreads();
       if (threadIdx.x == 0) sm.n_vict = 0;
+      PH(0);
       // ---- R2: |A|, new = |A \ S|; hits / misses; in-flight blocks leave the index ----
       uint32_t nA = 0, nnew = 0;
       uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_comp = 0, t_regen = 0;
       for (uint64_t wb = (P0 & ~31ull) + (uint64_t)wid * 32u; wb < P1; wb += (uint64_t)RT * UNR) {
-        uint32_t lf[UNR], uo[UNR], rp[UNR];
+        uint32_t lf[UNR], uo[UNR], rp[UNR], ru[UNR];
         bool in[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -467,7 +526,11 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           uo[u] = in[u] ? nd.u_of[pb] : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) rp[u] = (in[u] && !(lf[u] & LID_NFIE)) ? res_pos[lf[u] & LID_MASK] : NONE;
+        for (int u = 0; u < UNR; ++u) {
+          const bool first = in[u] && !(lf[u] & LID_NFIE);
+          rp[u] = first ? res_pos[lf[u] & LID_MASK] : NONE;
+          ru[u] = (first && !belady) ? res_unit[lf[u] & LID_MASK] : 0u;
+        }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           const bool first = in[u] && !(lf[u] & LID_NFIE);
@@ -487,7 +550,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             hb_update_warp(pend, resident, (uint32_t)(wb + (uint64_t)u * RT + lane), false);
           } else if (resident) {
             atomicAnd(&alive[rp[u] >> 5], ~(1u << (rp[u] & 31)));
-            atomicSub(&cnt[nd.u_of[rp[u]] & UMASK], 1u);
+            atomicSub(&cnt[ru[u]], 1u);
           }
         }
       }
@@ -502,6 +565,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       const uint32_t inAS = nA - nnew;  // in-flight (resident) blocks
       const int64_t kk = (pol == SAGA_POLICY_EVICT_ALL) ? (int64_t)S - (int64_t)inAS
                                                         : (int64_t)S + (int64_t)nnew - (int64_t)C;
+      PH(1);
       // ---- R3: evict the k largest keys among cand = S \ A ----
       if (kk > 0) {
         const uint32_t k = (uint32_t)kk;
@@ -511,32 +575,31 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         if (belady) {
           // in-flight blocks left `pend` in R2 (their next use is this epoch)
           const uint32_t nd_ = sm.tot_dead, np_ = sm.tot_pend - inAS;
+          if (threadIdx.x == 0 && sm.tot_pend < inAS) dbg_fail(a.dbg, __LINE__, sm.tot_pend, inAS, e);
           if (k <= nd_) {
-            hb_take_top(dead, k, vlist, VT_LID, sm);
+            hb_take_top(dead, k, vlist, VT_LID, sm, a.dbg);
           } else {
             if (nd_ > 0) hb_take_from(dead, 0, 0, 0, vlist, &sm.n_vict, VT_LID);
-            if (k - nd_ <= np_) { __syncthreads(); hb_take_top(pend, k - nd_, vlist, 0u, sm); }
-            else bad = 1;
+            __syncthreads();
+            if (k - nd_ <= np_) hb_take_top(pend, k - nd_, vlist, 0u, sm, a.dbg);
+            else { bad = 1; if (threadIdx.x == 0) dbg_fail(a.dbg, __LINE__, k, nd_, np_); }
           }
+          __syncthreads();
           if (threadIdx.x == 0) {
             sm.tot_dead = nd_ - min(k, nd_);
             sm.tot_pend = np_ - (k > nd_ ? k - nd_ : 0u);
           }
         } else {
-          const uint32_t* L = lists[cur];
+          ListRec* L = lists[cur];
           // whole-unit eviction: list every resident latest position of unit u (warp-collective)
-          auto evict_unit = [&](uint32_t u, bool prot) {
-            const uint32_t pa = nd.u_pos[u], pe = nd.u_pos[u + 1];
+          auto evict_unit = [&](uint32_t u, uint32_t pa, uint32_t pe, bool prot) {
             const uint32_t wlast = (pe - 1) >> 5;
             uint32_t taken = 0;
             for (uint32_t wb = pa >> 5; wb <= wlast; wb += 32) {
               const uint32_t wi = wb + lane;
               uint32_t wv = 0;
               if (wi <= wlast) {
-                uint32_t m = 0xffffffffu;
-                if (wi == (pa >> 5)) m &= ~((1u << (pa & 31)) - 1u);
-                if (wi == wlast && (pe & 31)) m &= (1u << (pe & 31)) - 1u;
-                wv = alive[wi] & m;
+                wv = alive[wi] & unit_mask(wi, pa, pe);
                 if (wv) atomicAnd(&alive[wi], ~wv);
               }
               emit_bits(vlist, &sm.n_vict, wi, wv, 0u);
@@ -547,18 +610,19 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           };
           if (!aeg) {  // EVICT_ALL: every candidate
             for (uint32_t i = wid; i < nL; i += RW) {
-              const uint32_t u = L[i];
-              if (cnt[u]) evict_unit(u, false);
+              const ListRec r = L[i];
+              if (cnt[r.u]) evict_unit(r.u, r.pa, r.pe, false);
             }
           } else {
             // pass a: normalisers over cand (eq:recency tau_max, eq:size size_max)
             long long tau = 0;
             uint32_t smax = 1;
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
-              const uint32_t u = L[i];
-              if (!cnt[u]) continue;
-              tau = max(tau, (long long)(Te - nd.u_t[u]));
-              smax = max(smax, owner_size(v, sstate, nd.u_own[u]));
+              const ListRec r = L[i];
+              if (!cnt[r.u]) continue;
+              if (cnt[r.u] > r.pe - r.pa) dbg_fail(a.dbg, __LINE__, r.u, cnt[r.u], r.pe - r.pa);
+              tau = max(tau, (long long)(Te - r.t));
+              smax = max(smax, owner_size(v, ck, ocall, r.lo));
             }
             tau = block_reduce<RT, long long>(tau, Max(), sm.b, par);
             smax = block_reduce<RT, uint32_t>(smax, Max(), sm.b, par);
@@ -568,20 +632,21 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             x.num = min(x.den, max((int64_t)0, 1000 * (int64_t)S - (int64_t)a.p_low * C));
             x.ttl_max = a.ttl_max; x.alpha = a.alpha; x.beta = a.beta; x.gamma = a.gamma;
             const uint32_t act = nd.ev_act[j];
+            PH(2);
             // pass b: per-unit key part kp = (!prot << 31) | q, weighted histogram of the top digit
             for (uint32_t i = threadIdx.x; i < H1; i += RT) sm.hist[i] = 0;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
-              const uint32_t u = L[i];
-              const uint32_t c = cnt[u];
+              const ListRec r = L[i];
+              const uint32_t c = cnt[r.u];
               uint32_t kp = 0;
               if (c) {
-                const OwnerKeyIn oi = owner_in(v, sstate, nd.u_own[u], act);
-                const uint32_t q = quantize_q20(wa_lru_score(x, nd.u_t[u], oi.size, oi.P));
+                const OwnerKeyIn oi = owner_in(v, ck, ocall, r.lo, act);
+                const uint32_t q = quantize_q20(wa_lru_score(x, r.t, oi.size, oi.P));
                 kp = ((uint32_t)!ttl_protected(x, oi) << 31) | q;
                 atomicAdd(&sm.hist[((kp >> 31) << 11) | (q >> 10)], c);
               }
-              lkp[i] = kp;
+              L[i].kp = kp;
             }
             __syncthreads();
             uint32_t d1, r1, d2, r2;
@@ -589,9 +654,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             for (uint32_t i = threadIdx.x; i < 1024; i += RT) sm.hist[i] = 0;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
-              const uint32_t kp = lkp[i];
+              const uint32_t kp = L[i].kp;
               if ((((kp >> 31) << 11) | ((kp & 0x1FFFFFu) >> 10)) != d1) continue;
-              const uint32_t c = cnt[L[i]];
+              const uint32_t c = cnt[L[i].u];
               if (c) atomicAdd(&sm.hist[kp & 1023u], c);
             }
             __syncthreads();
@@ -601,22 +666,16 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             const bool whole = sm.hist[d2] == r2;  // the pivot units are evicted whole
             if (threadIdx.x == 0) sm.n_piv = 0;
             __syncthreads();
+            PH(3);
             // pass c: units above the pivot are evicted whole; pivot units are gathered by lid
             for (uint32_t i = wid; i < nL; i += RW) {
-              const uint32_t u = L[i];
-              const uint32_t kp = lkp[i];
-              if (!cnt[u] || kp < kps) continue;
-              if (kp > kps || whole) { evict_unit(u, !(kp >> 31)); continue; }
-              const uint32_t pa = nd.u_pos[u], pe = nd.u_pos[u + 1];
-              for (uint32_t wb = (pa >> 5); wb <= ((pe - 1) >> 5); wb += 32) {
+              const ListRec r = L[i];
+              if (!cnt[r.u] || r.kp < kps) continue;
+              if (r.kp > kps || whole) { evict_unit(r.u, r.pa, r.pe, !(r.kp >> 31)); continue; }
+              const uint32_t wlast = (r.pe - 1) >> 5;
+              for (uint32_t wb = (r.pa >> 5); wb <= wlast; wb += 32) {
                 const uint32_t wi = wb + lane;
-                uint32_t wv = 0;
-                if (wi <= ((pe - 1) >> 5)) {
-                  uint32_t m = 0xffffffffu;
-                  if (wi == (pa >> 5)) m &= ~((1u << (pa & 31)) - 1u);
-                  if (wi == ((pe - 1) >> 5) && (pe & 31)) m &= (1u << (pe & 31)) - 1u;
-                  wv = alive[wi] & m;
-                }
+                const uint32_t wv = wi <= wlast ? (alive[wi] & unit_mask(wi, r.pa, r.pe)) : 0u;
                 const uint32_t c = __popc(wv);
                 uint32_t xs = c;
 #pragma unroll
@@ -628,16 +687,21 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
                 uint32_t b0 = 0;
                 if (lane == 31 && tot) b0 = atomicAdd(&sm.n_piv, tot);
                 b0 = __shfl_sync(0xffffffffu, b0, 31) + xs - c;
-                for (uint32_t y = wv; y; y &= y - 1) kbuf[b0++] = wi * 32u + (uint32_t)(__ffs(y) - 1);
+                for (uint32_t y = wv; y; y &= y - 1) kbuf[b0++] = ((uint64_t)r.u << 32) | (wi * 32u + (uint32_t)(__ffs(y) - 1));
               }
             }
             __syncthreads();
             const uint32_t npv = sm.n_piv;
+            if (threadIdx.x == 0 && npv > C) dbg_fail(a.dbg, __LINE__, npv, C, r2);
             if (!whole && npv) {
-              // pivot keys differ only in lid: rank (lid << 32 | position) and keep the top r2
+              // pivot keys differ only in lid: rank (lid << 32 | slot) and keep the top r2
+              uint32_t* pslot = vlist + k;  // (unit, position) of gathered slot i, after the list
               for (uint32_t i = threadIdx.x; i < npv; i += RT) {
-                const uint32_t p = (uint32_t)kbuf[i];
-                kbuf[i] = ((uint64_t)(nd.lidf[p] & LID_MASK) << 32) | p;
+                const uint64_t g = kbuf[i];
+                const uint32_t p = (uint32_t)g;
+                pslot[2 * i] = (uint32_t)(g >> 32);
+                pslot[2 * i + 1] = p;
+                kbuf[i] = ((uint64_t)(nd.lidf[p] & LID_MASK) << 32) | i;
               }
               __syncthreads();
               const uint64_t T = radix_select<RT>(kbuf, npv, r2, sm.b, par);
@@ -645,9 +709,10 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
               for (uint32_t i = threadIdx.x; i < npv; i += RT) {
                 const uint64_t kv = kbuf[i];
                 if (kv < T) continue;
-                const uint32_t p = (uint32_t)kv, lid = (uint32_t)(kv >> 32);
+                const uint32_t sl = (uint32_t)kv, lid = (uint32_t)(kv >> 32);
+                const uint32_t u = pslot[2 * sl], p = pslot[2 * sl + 1];
                 atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
-                atomicSub(&cnt[nd.u_of[p] & UMASK], 1u);
+                atomicSub(&cnt[u], 1u);
                 res_pos[lid] = NONE;
                 hs += splitmix64(eh | lid);
                 ++tk;
@@ -658,8 +723,10 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           }
         }
         __syncthreads();
+        PH(4);
         // listed victims: positions (block at that position) or local ids (VT_LID)
         const uint32_t nvl = sm.n_vict;
+        if (threadIdx.x == 0 && nvl > k) dbg_fail(a.dbg, __LINE__, nvl, k, pol);
         for (uint32_t i = threadIdx.x; i < nvl; i += RT) {
           const uint32_t x = vlist[i];
           const uint32_t lid = (x & VT_LID) ? (x & ~VT_LID) : (nd.lidf[x] & LID_MASK);
@@ -670,10 +737,11 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             ((unsigned long long)n_direct << 32) | n_prot, Add(), sm.b, par);
         const uint32_t nv = nvl + (uint32_t)(nvp >> 32), np = (uint32_t)nvp;
         hash += hs;
-        if (nv != k) bad = 1;
+        if (nv != k) { bad = 1; if (threadIdx.x == 0) dbg_fail(a.dbg, __LINE__, nv, k, pol); }
         S -= nv;
         c_ev += nv; c_prot += aeg ? np : 0; c_evev += 1;  // uniform
       }
+      PH(5);
       // ---- R4: the last record of each block in the epoch re-enters the index ----
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -708,6 +776,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             if (lane == 0 && wv) atomicOr(&alive[(wb + (uint64_t)u * RT) >> 5], wv);
             const uint32_t un = uo[u] & UMASK;
             if (last[u]) {
+              res_unit[lid] = un;
               const uint32_t pr = __match_any_sync(wv, un);
               if (lane == 31 - __clz(pr)) atomicAdd(&cnt[un], (uint32_t)__popc(pr));
             }
@@ -715,30 +784,38 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         }
       }
       S += nnew;
+      PH(6);
       // ---- live unit list: keep units with cnt > 0, append this epoch's units ----
       if (!belady) {
         __syncthreads();
-        const uint32_t* L = lists[cur];
-        uint32_t* L2 = lists[cur ^ 1];
+        const ListRec* L = lists[cur];
+        ListRec* L2 = lists[cur ^ 1];
         const uint32_t U0 = nd.ev_unit[j], U1 = nd.ev_unit[j + 1];
         const uint32_t tot = nL + (U1 - U0);
         for (uint32_t i = threadIdx.x; i < ((tot + 31) & ~31u); i += RT) {
-          uint32_t u = 0;
+          ListRec r{};
           bool keep = false;
           if (i < tot) {
-            u = i < nL ? L[i] : U0 + (i - nL);
-            keep = cnt[u] != 0;
+            if (i < nL) {
+              r = L[i];
+            } else {
+              const uint32_t u = U0 + (i - nL);
+              const UnitRec ur = nd.urec[u];
+              r.t = ur.t; r.u = u; r.pa = ur.pa; r.pe = ur.pe; r.lo = ur.lo; r.kp = 0; r.pad = 0;
+            }
+            keep = cnt[r.u] != 0;
           }
           const uint32_t km = __ballot_sync(0xffffffffu, keep);
           uint32_t b0 = 0;
           if (lane == 0 && km) b0 = atomicAdd(&sm.n_app, (uint32_t)__popc(km));
           b0 = __shfl_sync(0xffffffffu, b0, 0);
-          if (keep) L2[b0 + __popc(km & ((1u << lane) - 1u))] = u;
+          if (keep) L2[b0 + __popc(km & ((1u << lane) - 1u))] = r;
         }
         __syncthreads();
         nL = sm.n_app;
         cur ^= 1;
       }
+      PH(7);
       c_peak = max(c_peak, (long long)S);
       c_events += 1;
     }
@@ -776,14 +853,28 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       out[SAGA_C_PEAK_RESIDENT] = c_peak;
       out[SAGA_C_EVENT_EPOCHS] = c_events;
       if (a.item_cyc) a.item_cyc[it] = (unsigned long long)(clock64() - t_start);
+      if (a.phase_cyc)
+        for (int i = 0; i < 8; ++i) a.phase_cyc[(uint64_t)it * 8 + i] = (unsigned long long)ph[i];
     }
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// replay index of a node (built once): event positions, units, session-update ranges
+// replay index of a node (built once): event positions, units, local owners, update ranges
 // ------------------------------------------------------------------------------------------
+__global__ void k_call_key(TraceView v, CallKey* ck) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < v.n_calls; c += gridDim.x * blockDim.x) {
+    CallKey k;
+    k.tend = v.tend[c];
+    k.P = v.ci_P[c];
+    k.size = v.ci_size[c];
+    k.ttl = (uint32_t)v.ttl[v.call_v[c]];
+    k.fin = v.ci_fin[c];
+    ck[c] = k;
+  }
+}
+
 __global__ void k_ev_pos(const uint64_t* g_pos, const uint32_t* ev_g, uint32_t J, uint64_t* ev_pos) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= J; j += gridDim.x * blockDim.x) ev_pos[j] = g_pos[ev_g[j]];
 }
@@ -797,20 +888,38 @@ __global__ void k_group_head(const uint64_t* g_pos, uint32_t G, uint32_t* head) 
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x)
     if (g_pos[g] < g_pos[g + 1]) head[g_pos[g]] = 1u;
 }
-// hpos = exclusive scan of head: unit of p = hpos[p+1] - 1
+// private owners present at the node -> dense local ids
+__global__ void k_owner_flag(const uint32_t* lown, uint32_t n_local, uint32_t n_sessions, uint32_t* flag) {
+  for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_local; l += gridDim.x * blockDim.x) {
+    const uint32_t o = lown[l];
+    if (o < n_sessions) flag[o] = 1u;
+  }
+}
+// hpos = exclusive scan of head: the unit of p is hpos[p+1] - 1
 __global__ void k_unit_fill(const uint32_t* head, const uint32_t* hpos, uint64_t N, const uint32_t* lidf,
                             const uint32_t* lown, const uint64_t* g_pos, uint32_t G, const int64_t* g_t,
-                            const uint32_t* g_kind, uint32_t* u_pos, int64_t* u_t, uint32_t* u_own, uint32_t* u_kind) {
+                            const uint32_t* g_kind, const uint32_t* s2lo, uint32_t n_sessions, uint32_t* u_pos,
+                            UnitRec* urec, uint32_t* u_kind) {
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
     if (!head[p]) continue;
     const uint32_t u = hpos[p];
     uint32_t lo = 0, hi = G;  // last group with g_pos[g] <= p
     while (lo + 1 < hi) { const uint32_t mid = (lo + hi) >> 1; if (g_pos[mid] <= p) lo = mid; else hi = mid; }
+    const uint32_t own = lown[lidf[p] & LID_MASK];
     u_pos[u] = (uint32_t)p;
-    u_t[u] = g_t[lo];
-    u_own[u] = lown[lidf[p] & LID_MASK];
+    UnitRec r;
+    r.t = g_t[lo];
+    r.pa = (uint32_t)p;
+    r.pe = 0;
+    r.lo = own < n_sessions ? s2lo[own] : (LO_SHARED | (own - n_sessions));
+    r.pad = 0;
+    urec[u] = r;
     u_kind[u] = g_kind[lo];
   }
+}
+__global__ void k_unit_end(const uint32_t* u_pos, uint32_t n_units, uint64_t N, UnitRec* urec) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += gridDim.x * blockDim.x)
+    urec[u].pe = u + 1 < n_units ? u_pos[u + 1] : (uint32_t)N;
 }
 __global__ void k_unit_of(const uint32_t* hpos, uint64_t N, const uint32_t* u_kind, uint32_t* u_of) {
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
@@ -819,8 +928,8 @@ __global__ void k_unit_of(const uint32_t* hpos, uint64_t N, const uint32_t* u_ki
   }
 }
 __global__ void k_ev_index(TraceView v, const uint64_t* ev_pos, const uint32_t* ev_e, uint32_t J, const uint32_t* hpos,
-                           uint64_t N, uint32_t n_units, const uint32_t* upd_c, uint32_t n_upd, uint32_t* ev_unit,
-                           uint32_t* ev_upd, uint32_t* u_pos, uint64_t* N_out_unused, uint32_t* max_ev_units) {
+                           uint64_t N, uint32_t n_units, const uint32_t* upd_c, uint32_t n_upd, const uint32_t* s2lo,
+                           uint32_t* ev_unit, uint32_t* ev_upd, uint32_t* upd_lo) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= J; j += gridDim.x * blockDim.x) {
     const uint64_t p = ev_pos[j];
     ev_unit[j] = p < N ? hpos[p] : n_units;
@@ -829,12 +938,10 @@ __global__ void k_ev_index(TraceView v, const uint64_t* ev_pos, const uint32_t* 
       uint32_t lo = 0, hi = n_upd;  // #updates with e(c) <= e
       while (lo < hi) { const uint32_t mid = (lo + hi) >> 1; if (v.ecall[upd_c[mid]] <= e) lo = mid + 1; else hi = mid; }
       ev_upd[j] = lo;
-      const uint64_t p1 = ev_pos[j + 1];
-      const uint32_t u1 = p1 < N ? hpos[p1] : n_units;
-      atomicMax(max_ev_units, u1 - ev_unit[j]);
     }
-    if (j == 0) u_pos[n_units] = (uint32_t)N;
   }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_upd; i += gridDim.x * blockDim.x)
+    upd_lo[i] = s2lo[v.call_sess[upd_c[i]]];
 }
 
 unsigned grid_for(uint64_t n, int threads = NTHREADS) {
@@ -847,57 +954,64 @@ unsigned grid_for(uint64_t n, int threads = NTHREADS) {
 saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   NodeDev& nd = t->nodes[w];
   if (nd.rp_done) return SAGA_OK;
+  const TraceView& v = t->v;
   const uint64_t N = nd.N;
   const uint32_t J = nd.J;
-  uint32_t* head = nullptr;
-  uint32_t* hpos = nullptr;
-  uint32_t* u_kind = nullptr;
-  uint32_t* dmax = nullptr;
+  const uint32_t NS = std::max(v.n_sessions, 1u);
+  uint32_t *head = nullptr, *hpos = nullptr, *u_kind = nullptr, *u_pos = nullptr, *sflag = nullptr, *s2lo = nullptr;
   SAGA_CK(ws_malloc((void**)&head, (N + 1) * 4, s));
   SAGA_CK(ws_malloc((void**)&hpos, (N + 2) * 4, s));
-  SAGA_CK(ws_malloc((void**)&dmax, 4, s));
-  SAGA_CK(cudaMemsetAsync(dmax, 0, 4, s));
+  SAGA_CK(ws_malloc((void**)&sflag, (size_t(NS) + 1) * 4, s));
+  SAGA_CK(ws_malloc((void**)&s2lo, (size_t(NS) + 1) * 4, s));
+  SAGA_CK(cudaMemsetAsync(sflag, 0, (size_t(NS) + 1) * 4, s));
   nd.ev_pos = dalloc<uint64_t>(t, size_t(J) + 1);
   nd.u_of = dalloc<uint32_t>(t, N);
   if (!nd.ev_pos || !nd.u_of) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
   k_ev_pos<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(nd.g_pos, nd.ev_g, J, nd.ev_pos);
   count_launch();
+  if (nd.n_local) {
+    k_owner_flag<<<grid_for(nd.n_local), NTHREADS, 0, s>>>(nd.lown, nd.n_local, v.n_sessions, sflag);
+    count_launch();
+  }
+  SAGA_CK(scan_u32(t, sflag, s2lo, NS));
   if (N > 0) {
     k_unit_head<<<grid_for(N), NTHREADS, 0, s>>>(nd.lidf, nd.lown, N, head);
     if (nd.G) k_group_head<<<grid_for(nd.G), NTHREADS, 0, s>>>(nd.g_pos, nd.G, head);
     count_launch(2);
   }
   SAGA_CK(scan_u32(t, head, hpos, N));
-  uint32_t nu = 0;
-  SAGA_CK(cudaMemcpyAsync(&nu, hpos + N, 4, cudaMemcpyDeviceToHost, s));
+  uint32_t hv[2] = {0, 0};
+  SAGA_CK(cudaMemcpyAsync(&hv[0], hpos + N, 4, cudaMemcpyDeviceToHost, s));
+  SAGA_CK(cudaMemcpyAsync(&hv[1], s2lo + NS, 4, cudaMemcpyDeviceToHost, s));
   SAGA_CK(cudaStreamSynchronize(s));
+  const uint32_t nu = hv[0];
   nd.n_units = nu;
-  // hpos[N] = n_units is read by k_unit_of as hpos[p + 1] for p = N - 1
-  nd.u_pos = dalloc<uint32_t>(t, size_t(nu) + 1);
-  nd.u_t = dalloc<int64_t>(t, nu);
-  nd.u_own = dalloc<uint32_t>(t, nu);
+  nd.n_lo = hv[1];
+  nd.urec = dalloc<UnitRec>(t, nu);
   nd.ev_unit = dalloc<uint32_t>(t, size_t(J) + 1);
   nd.ev_upd = dalloc<uint32_t>(t, J);
+  nd.upd_lo = dalloc<uint32_t>(t, nd.n_upd);
   SAGA_CK(ws_malloc((void**)&u_kind, (size_t(nu) + 1) * 4, s));
-  if (!nd.u_pos || !nd.u_t || !nd.u_own || !nd.ev_unit || !nd.ev_upd) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
+  SAGA_CK(ws_malloc((void**)&u_pos, (size_t(nu) + 1) * 4, s));
+  if (!nd.urec || !nd.ev_unit || !nd.ev_upd || !nd.upd_lo) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
   if (N > 0) {
-    k_unit_fill<<<grid_for(N), NTHREADS, 0, s>>>(head, hpos, N, nd.lidf, nd.lown, nd.g_pos, nd.G, nd.g_t, nd.g_kind,
-                                                 nd.u_pos, nd.u_t, nd.u_own, u_kind);
+    UnitRec* ur = static_cast<UnitRec*>(nd.urec);
+    k_unit_fill<<<grid_for(N), NTHREADS, 0, s>>>(head, hpos, N, nd.lidf, nd.lown, nd.g_pos, nd.G, nd.g_t, nd.g_kind, s2lo,
+                                                 v.n_sessions, u_pos, ur, u_kind);
+    k_unit_end<<<grid_for(nu), NTHREADS, 0, s>>>(u_pos, nu, N, ur);
     k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(hpos, N, u_kind, nd.u_of);
-    count_launch(2);
+    count_launch(3);
   }
-  k_ev_index<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(t->v, nd.ev_pos, nd.ev_e, J, hpos, N, nu, nd.upd_c, nd.n_upd,
-                                                          nd.ev_unit, nd.ev_upd, nd.u_pos, nullptr, dmax);
+  k_ev_index<<<grid_for(std::max<size_t>(size_t(J) + 1, nd.n_upd)), NTHREADS, 0, s>>>(
+      v, nd.ev_pos, nd.ev_e, J, hpos, N, nu, nd.upd_c, nd.n_upd, s2lo, nd.ev_unit, nd.ev_upd, nd.upd_lo);
   count_launch();
-  uint32_t hm = 0;
-  SAGA_CK(cudaMemcpyAsync(&hm, dmax, 4, cudaMemcpyDeviceToHost, s));
   SAGA_CK_LAUNCH();
-  SAGA_CK(cudaStreamSynchronize(s));
-  nd.max_ev_units = hm;
   ws_free(head, s);
   ws_free(hpos, s);
   ws_free(u_kind, s);
-  ws_free(dmax, s);
+  ws_free(u_pos, s);
+  ws_free(sflag, s);
+  ws_free(s2lo, s);
   nd.rp_done = true;
   return SAGA_OK;
 }
@@ -913,7 +1027,15 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   if (n_caps > 0xFFFFu || n_owned > 0xFFFu) { set_error("saga_replay: at most 65535 capacities and 4095 nodes per call"); return SAGA_ERR_INVALID_ARG; }
   uint32_t cap_max = 0;
   for (uint32_t i = 0; i < n_caps; ++i) cap_max = std::max(cap_max, caps[i]);
-  uint64_t max_local = 1, maxN = 1, max_units = 1;
+  if (!t->callkey) {
+    t->callkey = dalloc<CallKey>(t, v.n_calls);
+    if (!t->callkey) { set_error("out of device memory (replay)"); return SAGA_ERR_OOM; }
+    if (v.n_calls) {
+      k_call_key<<<grid_for(v.n_calls), NTHREADS, 0, s>>>(v, static_cast<CallKey*>(t->callkey));
+      count_launch();
+    }
+  }
+  uint64_t max_local = 1, maxN = 1, max_units = 1, max_lo = 1;
   for (uint32_t i = 0; i < n_owned; ++i) {
     saga_status st = build_replay_index(t, nodes[i], s);
     if (st != SAGA_OK) return st;
@@ -921,15 +1043,16 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
     max_local = std::max<uint64_t>(max_local, nd.n_local);
     maxN = std::max<uint64_t>(maxN, nd.N);
     max_units = std::max<uint64_t>(max_units, nd.n_units);
+    max_lo = std::max<uint64_t>(max_lo, nd.n_lo);
   }
   std::vector<NodeArr> hn(t->n_nodes);
   for (uint32_t w = 0; w < t->n_nodes; ++w) {
     const NodeDev& nd = t->nodes[w];
     NodeArr x{};
-    x.N = nd.N; x.J = nd.J; x.n_local = nd.n_local; x.n_units = nd.n_units;
+    x.N = nd.N; x.J = nd.J; x.n_local = nd.n_local; x.n_units = nd.n_units; x.n_lo = nd.n_lo;
     x.ev_pos = nd.ev_pos; x.ev_e = nd.ev_e; x.ev_inv = nd.ev_inv; x.ev_act = nd.ev_act; x.ev_unit = nd.ev_unit;
-    x.ev_upd = nd.ev_upd; x.inv_s = nd.inv_s; x.lidf = nd.lidf; x.nxt = nd.nxt; x.u_of = nd.u_of; x.u_pos = nd.u_pos;
-    x.u_t = nd.u_t; x.u_own = nd.u_own; x.lid2gid = nd.lid2gid; x.upd_c = nd.upd_c;
+    x.ev_upd = nd.ev_upd; x.inv_s = nd.inv_s; x.lidf = nd.lidf; x.nxt = nd.nxt; x.u_of = nd.u_of;
+    x.urec = static_cast<const UnitRec*>(nd.urec); x.lid2gid = nd.lid2gid; x.upd_c = nd.upd_c; x.upd_lo = nd.upd_lo;
     hn[w] = x;
   }
   // items, largest capacity first (the per-event cost grows with |S| <= C)
@@ -949,26 +1072,38 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   ReplayArgs a{};
   uint64_t off = 0;
   a.o_res = off; off += al(max_local * 4 + 16);
+  a.o_runit = off; off += al(max_local * 4 + 16);
   a.o_bits = off; off += al(n2N * 32768 * 4);
   a.o_c1 = off; off += al(n2N * 1024 * 4);
   a.o_dbits = off; off += al(n2L * 32768 * 4);
   a.o_dc1 = off; off += al(n2L * 1024 * 4);
   a.o_cnt = off; off += al(max_units * 4);
-  a.o_list0 = off; off += al(max_units * 4);
-  a.o_list1 = off; off += al(max_units * 4);
-  a.o_lkp = off; off += al(max_units * 4);
+  a.o_list0 = off; off += al(max_units * sizeof(ListRec));
+  a.o_list1 = off; off += al(max_units * sizeof(ListRec));
   a.o_kbuf = off; off += al(((uint64_t)cap_max + 1) * 8);
-  a.o_vl = off; off += al(((uint64_t)cap_max + 1) * 4);
-  a.o_sst = off; off += al((uint64_t)std::max(v.n_sessions, 1u) * 4);
+  a.o_vl = off; off += al(((uint64_t)cap_max + 1) * 12);  // victim list + pivot (unit, position) pairs
+  a.o_ocall = off; off += al(max_lo * 4);
   a.cta_bytes = off;
-  // dynamic shared memory: the c2 counts always; the c1 counts (BELADY) and the unit counts
-  // (AEG / EVICT_ALL; same region) when they fit
-  const uint64_t dyn_max = 160ull * 1024;
+  // dynamic shared memory (one CTA per SM):
+  //   BELADY: c2 counts of both bitmaps, then their c1 counts, then the dead bits, while they fit;
+  //   AEG / EVICT_ALL: the newest-call table, then the unit counts, while they fit.
+  // the rest of the 228 KB unified L1/shared array stays L1 cache, which the per-event loads need
+  uint64_t dyn_max = 64ull * 1024;
+  if (const char* e = getenv("SAGA_REPLAY_SMEM_KB")) dyn_max = std::max<uint64_t>(1, strtoull(e, nullptr, 10)) * 1024;
+  dyn_max = std::min<uint64_t>(dyn_max, 200ull * 1024);
   const uint64_t c2_bytes = ((n2N + n2L + 3) & ~3ull) * 4;
   const uint64_t c1_bytes = (n2N + n2L) * 1024 * 4;
+  const uint64_t db_bytes = ((max_local + 1023) >> 10) * 32 * 4;
   a.n2N_max = (uint32_t)n2N; a.n2L_max = (uint32_t)n2L;
   a.dyn_c1 = (c2_bytes + c1_bytes <= dyn_max) ? 1u : 0u;
-  uint64_t dyn = std::max<uint64_t>(a.dyn_c1 ? c2_bytes + c1_bytes : c2_bytes, std::min<uint64_t>(max_units * 4, dyn_max));
+  uint64_t dyn_b = a.dyn_c1 ? c2_bytes + c1_bytes : c2_bytes;
+  if (dyn_b + db_bytes <= dyn_max) { a.dyn_dbits_words = (uint32_t)(db_bytes / 4); dyn_b += db_bytes; }
+  else a.dyn_dbits_words = 0;
+  const uint64_t oc_bytes = ((max_lo + 3) & ~3ull) * 4;
+  a.ocall_smem = oc_bytes <= 64 * 1024 ? 1u : 0u;
+  uint64_t dyn_a = (a.ocall_smem ? oc_bytes : 0) + max_units * 4;
+  dyn_a = std::min<uint64_t>(dyn_a, dyn_max);
+  uint64_t dyn = std::max<uint64_t>(std::max<uint64_t>(dyn_b, dyn_a), a.ocall_smem ? oc_bytes : 16);
   dyn = (dyn + 15) & ~15ull;
   a.dyn_words = (uint32_t)(dyn / 4);
   SAGA_CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
@@ -991,8 +1126,8 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   SAGA_CK(ws_malloc((void**)&d_caps, 4 * n_caps, s));
   SAGA_CK(ws_malloc((void**)&d_list, 4 * n_owned, s));
   SAGA_CK(ws_malloc((void**)&d_items, 4 * n_items, s));
-  SAGA_CK(ws_malloc((void**)&work, 8, s));
-  if (trace) SAGA_CK(ws_malloc((void**)&d_cyc, 8ull * n_items, s));
+  SAGA_CK(ws_malloc((void**)&work, 32, s));
+  if (trace) SAGA_CK(ws_malloc((void**)&d_cyc, 8ull * 9 * n_items, s));
   if (ws_malloc((void**)&scratch, a.cta_bytes * grid, s) != cudaSuccess) {
     set_error("out of device memory (replay scratch %llu bytes)", (unsigned long long)(a.cta_bytes * grid));
     return SAGA_ERR_OOM;
@@ -1001,39 +1136,48 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   SAGA_CK(cudaMemcpyAsync(d_caps, caps, 4 * n_caps, cudaMemcpyHostToDevice, s));
   SAGA_CK(cudaMemcpyAsync(d_list, nodes, 4 * n_owned, cudaMemcpyHostToDevice, s));
   SAGA_CK(cudaMemcpyAsync(d_items, items.data(), 4 * n_items, cudaMemcpyHostToDevice, s));
-  SAGA_CK(cudaMemsetAsync(work, 0, 8, s));
+  SAGA_CK(cudaMemsetAsync(work, 0, 32, s));
   a.v = v;
   a.nodes = d_nodes; a.caps = d_caps; a.items = d_items; a.n_items = n_items; a.node_list = d_list;
   a.pol[0] = pol[0]; a.pol[1] = n_pol > 1 ? pol[1] : 0; a.pol[2] = n_pol > 2 ? pol[2] : 0;
   a.n_caps = n_caps; a.n_nodes_total = t->n_nodes; a.counters = counters;
   a.alpha = cfg->alpha; a.beta = cfg->beta; a.gamma = cfg->gamma;
   a.p_low = cfg->p_low_pm; a.p_high = cfg->p_high_pm; a.ttl_max = cfg->ttl_max_us;
-  a.scratch = scratch; a.work = work; a.err = work + 1; a.item_cyc = d_cyc;
+  a.callkey = static_cast<const CallKey*>(t->callkey);
+  a.scratch = scratch; a.work = work; a.err = work + 1; a.dbg = work + 4; a.item_cyc = d_cyc;
+  a.phase_cyc = d_cyc ? d_cyc + n_items : nullptr;
   prof_begin(SAGA_PROF_REPLAY, s);
   k_replay<<<grid, RT, dyn, s>>>(a);
   prof_end(SAGA_PROF_REPLAY, s);
   count_launch();
   SAGA_CK_LAUNCH();
-  uint32_t herr = 0;
-  SAGA_CK(cudaMemcpyAsync(&herr, work + 1, 4, cudaMemcpyDeviceToHost, s));
-  std::vector<unsigned long long> cyc(trace ? n_items : 0);
-  if (trace) SAGA_CK(cudaMemcpyAsync(cyc.data(), d_cyc, 8ull * n_items, cudaMemcpyDeviceToHost, s));
+  uint32_t hw[8] = {0};
+  SAGA_CK(cudaMemcpyAsync(hw, work, 32, cudaMemcpyDeviceToHost, s));
+  const uint32_t& herr = hw[1];
+  std::vector<unsigned long long> cyc(trace ? 9ull * n_items : 0);
+  if (trace) SAGA_CK(cudaMemcpyAsync(cyc.data(), d_cyc, 8ull * 9 * n_items, cudaMemcpyDeviceToHost, s));
   ws_free(d_nodes, s); ws_free(d_caps, s); ws_free(d_list, s); ws_free(d_items, s);
   ws_free(scratch, s);
   ws_free(work, s);
   if (d_cyc) ws_free(d_cyc, s);
   SAGA_CK(cudaStreamSynchronize(s));
   if (trace) {
-    fprintf(stderr, "[saga replay] grid %u x %d threads, dyn smem %llu B (c1 %s), %u items\n", grid, RT,
-            (unsigned long long)dyn, a.dyn_c1 ? "smem" : "global", n_items);
+    fprintf(stderr, "[saga replay] grid %u x %d threads, dyn smem %llu B (c1 %s, dead bits %s, ocall %s), %u items\n",
+            grid, RT, (unsigned long long)dyn, a.dyn_c1 ? "smem" : "global", a.dyn_dbits_words ? "smem" : "global",
+            a.ocall_smem ? "smem" : "global", n_items);
     for (uint32_t i = 0; i < n_items; ++i) {
       const uint32_t pk = items[i];
       const uint32_t w = nodes[pk & 0xFFFu];
-      fprintf(stderr, "[saga replay] item pol=%u cap=%u node=%u events=%u Mcycles=%.2f\n", pol[pk >> 28],
-              caps[(pk >> 12) & 0xFFFFu], w, t->nodes[w].J, cyc[i] / 1e6);
+      const unsigned long long* ph = &cyc[n_items + 8ull * i];
+      fprintf(stderr, "[saga replay] item pol=%u cap=%u node=%u events=%u units=%u Mcycles=%.2f phases=%.1f,%.1f,%.1f,%.1f,%.1f,%.1f,%.1f,%.1f\n",
+              pol[pk >> 28], caps[(pk >> 12) & 0xFFFFu], w, t->nodes[w].J, t->nodes[w].n_units, cyc[i] / 1e6,
+              ph[0] / 1e6, ph[1] / 1e6, ph[2] / 1e6, ph[3] / 1e6, ph[4] / 1e6, ph[5] / 1e6, ph[6] / 1e6, ph[7] / 1e6);
     }
   }
-  if (herr) { set_error("saga_replay: internal selection check failed"); return SAGA_ERR_STATE; }
+  if (herr || hw[4]) {
+    set_error("saga_replay: internal selection check failed (k_replay.cu:%u values %u %u %u)", hw[4], hw[5], hw[6], hw[7]);
+    return SAGA_ERR_STATE;
+  }
   return SAGA_OK;
 }
 

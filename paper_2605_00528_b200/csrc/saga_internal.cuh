@@ -120,9 +120,9 @@ struct NodeDev {
   uint32_t* ev_unit = nullptr; // [J+1] first unit of event j
   uint32_t* ev_upd = nullptr;  // [J] end of the session-update list for event j
   uint32_t* u_of = nullptr;    // [N] unit of position p | KIND_MIG
-  uint32_t* u_pos = nullptr;   // [n_units+1] first position of unit u
-  int64_t* u_t = nullptr;      // [n_units] t of the unit's record group (t_c or T_e for MIG)
-  uint32_t* u_own = nullptr;   // [n_units] owner of the unit's blocks
+  void* urec = nullptr;        // [n_units] UnitRec (k_replay.cu): t, position range, local owner
+  uint32_t n_lo = 0;           // private owners (sessions) with blocks at this node
+  uint32_t* upd_lo = nullptr;  // [n_upd] local owner id of each session-update call
 };
 
 }  // namespace saga
@@ -143,6 +143,7 @@ struct saga_trace {
   uint32_t n_mig = 0, n_act = 0;
   int64_t n_steals = 0, n_reroutes = 0;
   std::vector<saga::NodeDev> nodes;
+  void* callkey = nullptr;          // [n_calls] CallKey (k_replay.cu), built by the first replay
   std::vector<void*> allocs;        // every device allocation owned by the handle
 };
 
