@@ -87,6 +87,8 @@ struct NodeArr {
   const uint32_t* lidf;
   const uint32_t* nxt;
   const uint32_t* u_of;
+  const uint32_t* prv;
+  const uint32_t* upu;
   const UnitRec* urec;
   const uint32_t* lid2gid;
   const uint32_t* upd_c;
@@ -111,7 +113,7 @@ struct ReplayArgs {
   uint8_t* scratch;
   uint64_t cta_bytes;
   const CallKey* callkey;
-  uint64_t o_res, o_runit, o_bits, o_c1, o_dbits, o_dc1, o_cnt, o_list0, o_list1, o_kbuf, o_vl, o_ocall;
+  uint64_t o_res, o_nres, o_bits, o_c1, o_dbits, o_dc1, o_cnt, o_list0, o_list1, o_kbuf, o_vl, o_vu, o_ocall;
   uint32_t n2N_max, n2L_max;   // c2 entries of the two bitmaps (dynamic shared memory)
   uint32_t dyn_c1;             // BELADY: the c1 arrays are in dynamic shared memory too
   uint32_t dyn_dbits_words;    // BELADY: dead bits in shared memory when n_local <= 32 * this
@@ -129,7 +131,7 @@ struct Smem {
   uint32_t hist[H1];
   uint32_t res_j, res_rem, thr, item;
   uint32_t hb_j2, hb_j1;
-  uint32_t n_app, n_piv, n_vict;
+  uint32_t n_app, n_piv, n_vict, n_vu;
   uint32_t ilo, ihi;
   uint32_t tot_dead, tot_pend;  // BELADY: set bits of the two hierarchical bitmaps
 };
@@ -398,8 +400,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* base = a.scratch + (uint64_t)blockIdx.x * a.cta_bytes;
   uint32_t* res_pos = reinterpret_cast<uint32_t*>(base + a.o_res);
-  uint32_t* res_unit = reinterpret_cast<uint32_t*>(base + a.o_runit);
   uint32_t* alive = reinterpret_cast<uint32_t*>(base + a.o_bits);   // AEG / EVICT_ALL (aliases pend.bits)
+  uint32_t* nres_a = reinterpret_cast<uint32_t*>(base + a.o_nres);  // AEG / EVICT_ALL next-use-resident bits
+  uint32_t* vunits = reinterpret_cast<uint32_t*>(base + a.o_vu);    // AEG: list entries evicted this epoch
   ListRec* lists[2] = {reinterpret_cast<ListRec*>(base + a.o_list0), reinterpret_cast<ListRec*>(base + a.o_list1)};
   uint64_t* kbuf = reinterpret_cast<uint64_t*>(base + a.o_kbuf);
   uint32_t* vlist = reinterpret_cast<uint32_t*>(base + a.o_vl);
@@ -451,6 +454,8 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         for (uint32_t i = threadIdx.x; i < a.n2N_max + a.n2L_max; i += RT) dyn[i] = 0;
         for (uint32_t i = threadIdx.x; i < n1L * 32u; i += RT) dbits[i] = 0;
       } else {
+        uint4* n4 = reinterpret_cast<uint4*>(nres_a);
+        for (uint32_t i = threadIdx.x; i < (uint32_t)((nd.N + 1023) / 1024) * 8u; i += RT) n4[i] = zero;
         for (uint32_t i = threadIdx.x; i < nd.n_units; i += RT) cnt[i] = 0;
         if (aeg) for (uint32_t i = threadIdx.x; i < nd.n_lo; i += RT) ocall[i] = 0;
       }
@@ -499,7 +504,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             else { hb_clear(pend, q); atomicSub(&sm.tot_pend, 1u); }
           } else {
             atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
-            atomicSub(&cnt[res_unit[l]], 1u);
+            atomicSub(&cnt[nd.u_of[p] & UMASK], 1u);
+            const uint32_t q = nd.nxt[p];
+            if (q != INF32) atomicAnd(&nres_a[q >> 5], ~(1u << (q & 31)));
           }
         }
         nrm = block_reduce<RT, uint32_t>(nrm, Add(), sm.b, par);
@@ -515,26 +522,28 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       // ---- R2: |A|, new = |A \ S|; hits / misses; in-flight blocks leave the index ----
       uint32_t nA = 0, nnew = 0;
       uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_comp = 0, t_regen = 0;
+      // A first-in-epoch record p is a hit iff bit p of the next-use-resident bitmap is set (the
+      // resident block's next use is p); a warp's 32 positions are one aligned bitmap word.
+      uint32_t* nres = belady ? pend.bits : nres_a;
       for (uint64_t wb = (P0 & ~31ull) + (uint64_t)wid * 32u; wb < P1; wb += (uint64_t)RT * UNR) {
-        uint32_t lf[UNR], uo[UNR], rp[UNR], ru[UNR];
+        uint32_t lf[UNR], uo[UNR], pv[UNR], up[UNR], nw[UNR];
         bool in[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          const uint64_t pb = wb + (uint64_t)u * RT + lane;
+          const uint64_t wbu = wb + (uint64_t)u * RT;
+          const uint64_t pb = wbu + lane;
           in[u] = pb >= P0 && pb < P1;
           lf[u] = in[u] ? nd.lidf[pb] : 0u;
           uo[u] = in[u] ? nd.u_of[pb] : 0u;
+          pv[u] = (in[u] && !belady) ? nd.prv[pb] : 0u;
+          up[u] = (in[u] && !belady) ? nd.upu[pb] : 0u;
+          nw[u] = wbu < P1 ? nres[wbu >> 5] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
+          const uint64_t wbu = wb + (uint64_t)u * RT;
           const bool first = in[u] && !(lf[u] & LID_NFIE);
-          rp[u] = first ? res_pos[lf[u] & LID_MASK] : NONE;
-          ru[u] = (first && !belady) ? res_unit[lf[u] & LID_MASK] : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const bool first = in[u] && !(lf[u] & LID_NFIE);
-          const bool resident = first && rp[u] != NONE;
+          const bool resident = first && ((nw[u] >> lane) & 1u);
           const bool mig = (uo[u] & KIND_MIG) != 0;
           if (in[u]) {
             if (first && !resident) {
@@ -546,11 +555,15 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
               if (mig) ++t_mhit; else ++t_hit;
             }
           }
-          if (belady) {
-            hb_update_warp(pend, resident, (uint32_t)(wb + (uint64_t)u * RT + lane), false);
-          } else if (resident) {
-            atomicAnd(&alive[rp[u] >> 5], ~(1u << (rp[u] & 31)));
-            atomicSub(&cnt[ru[u]], 1u);
+          // in-flight blocks leave the index until R4
+          const uint32_t rm = __ballot_sync(0xffffffffu, resident);
+          if (rm && lane == 0) {
+            atomicAnd(&nres[wbu >> 5], ~rm);
+            if (belady) { atomicSub(&pend.c1[wbu >> 10], (uint32_t)__popc(rm)); atomicSub(&pend.c2[wbu >> 20], (uint32_t)__popc(rm)); }
+          }
+          if (!belady && resident) {
+            atomicAnd(&alive[pv[u] >> 5], ~(1u << (pv[u] & 31)));
+            atomicSub(&cnt[up[u]], 1u);
           }
         }
       }
@@ -664,13 +677,24 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             const uint32_t kps = ((d1 >> 11) << 31) | ((d1 & 2047u) << 10) | d2;
             const bool prot_piv = !(kps >> 31);
             const bool whole = sm.hist[d2] == r2;  // the pivot units are evicted whole
-            if (threadIdx.x == 0) sm.n_piv = 0;
+            if (threadIdx.x == 0) { sm.n_piv = 0; sm.n_vu = 0; }
             __syncthreads();
             PH(3);
-            // pass c: units above the pivot are evicted whole; pivot units are gathered by lid
-            for (uint32_t i = wid; i < nL; i += RW) {
-              const ListRec r = L[i];
-              if (!cnt[r.u] || r.kp < kps) continue;
+            // pass c: list the entries with kp >= kp* (flat), then evict units above the pivot
+            // whole and gather the blocks of the pivot units by lid (a warp per listed entry)
+            for (uint32_t i = threadIdx.x; i < ((nL + 31) & ~31u); i += RT) {
+              bool vic = false;
+              if (i < nL) vic = L[i].kp >= kps && cnt[L[i].u] != 0;
+              const uint32_t vm = __ballot_sync(0xffffffffu, vic);
+              uint32_t b0 = 0;
+              if (lane == 0 && vm) b0 = atomicAdd(&sm.n_vu, (uint32_t)__popc(vm));
+              b0 = __shfl_sync(0xffffffffu, b0, 0);
+              if (vic) vunits[b0 + __popc(vm & ((1u << lane) - 1u))] = i;
+            }
+            __syncthreads();
+            const uint32_t nvu = sm.n_vu;
+            for (uint32_t q = wid; q < nvu; q += RW) {
+              const ListRec r = L[vunits[q]];
               if (r.kp > kps || whole) { evict_unit(r.u, r.pa, r.pe, !(r.kp >> 31)); continue; }
               const uint32_t wlast = (r.pe - 1) >> 5;
               for (uint32_t wb = (r.pa >> 5); wb <= wlast; wb += 32) {
@@ -713,6 +737,8 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
                 const uint32_t u = pslot[2 * sl], p = pslot[2 * sl + 1];
                 atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
                 atomicSub(&cnt[u], 1u);
+                const uint32_t qn = nd.nxt[p];
+                if (qn != INF32) atomicAnd(&nres_a[qn >> 5], ~(1u << (qn & 31)));
                 res_pos[lid] = NONE;
                 hs += splitmix64(eh | lid);
                 ++tk;
@@ -730,6 +756,10 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         for (uint32_t i = threadIdx.x; i < nvl; i += RT) {
           const uint32_t x = vlist[i];
           const uint32_t lid = (x & VT_LID) ? (x & ~VT_LID) : (nd.lidf[x] & LID_MASK);
+          if (!belady) {  // a victim's next use is no longer resident
+            const uint32_t qn = nd.nxt[x];
+            if (qn != INF32) atomicAnd(&nres_a[qn >> 5], ~(1u << (qn & 31)));
+          }
           res_pos[lid] = NONE;
           hs += splitmix64(eh | lid);
         }
@@ -776,7 +806,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             if (lane == 0 && wv) atomicOr(&alive[(wb + (uint64_t)u * RT) >> 5], wv);
             const uint32_t un = uo[u] & UMASK;
             if (last[u]) {
-              res_unit[lid] = un;
+              if (q[u] != INF32) atomicOr(&nres_a[q[u] >> 5], 1u << (q[u] & 31));
               const uint32_t pr = __match_any_sync(wv, un);
               if (lane == 31 - __clz(pr)) atomicAdd(&cnt[un], (uint32_t)__popc(pr));
             }
@@ -944,6 +974,20 @@ __global__ void k_ev_index(TraceView v, const uint64_t* ev_pos, const uint32_t* 
     upd_lo[i] = s2lo[v.call_sess[upd_c[i]]];
 }
 
+// previous occurrence of the block at each position (the inverse of next_use) and its unit
+__global__ void k_prev(const uint32_t* nxt, uint64_t N, uint32_t* prv) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = nxt[p];
+    if (q != INF32) prv[q] = (uint32_t)p;
+  }
+}
+__global__ void k_prev_unit(const uint32_t* prv, const uint32_t* u_of, uint64_t N, uint32_t* upu) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = prv[p];
+    upu[p] = q != NONE ? (u_of[q] & UMASK) : 0u;
+  }
+}
+
 unsigned grid_for(uint64_t n, int threads = NTHREADS) {
   uint64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -966,7 +1010,14 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   SAGA_CK(cudaMemsetAsync(sflag, 0, (size_t(NS) + 1) * 4, s));
   nd.ev_pos = dalloc<uint64_t>(t, size_t(J) + 1);
   nd.u_of = dalloc<uint32_t>(t, N);
-  if (!nd.ev_pos || !nd.u_of) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
+  nd.prv = dalloc<uint32_t>(t, N);
+  nd.upu = dalloc<uint32_t>(t, N);
+  if (!nd.ev_pos || !nd.u_of || !nd.prv || !nd.upu) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
+  SAGA_CK(cudaMemsetAsync(nd.prv, 0xFF, std::max<uint64_t>(N, 1) * 4, s));
+  if (N > 0) {
+    k_prev<<<grid_for(N), NTHREADS, 0, s>>>(nd.nxt, N, nd.prv);
+    count_launch();
+  }
   k_ev_pos<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(nd.g_pos, nd.ev_g, J, nd.ev_pos);
   count_launch();
   if (nd.n_local) {
@@ -1000,7 +1051,8 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
                                                  v.n_sessions, u_pos, ur, u_kind);
     k_unit_end<<<grid_for(nu), NTHREADS, 0, s>>>(u_pos, nu, N, ur);
     k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(hpos, N, u_kind, nd.u_of);
-    count_launch(3);
+    k_prev_unit<<<grid_for(N), NTHREADS, 0, s>>>(nd.prv, nd.u_of, N, nd.upu);
+    count_launch(4);
   }
   k_ev_index<<<grid_for(std::max<size_t>(size_t(J) + 1, nd.n_upd)), NTHREADS, 0, s>>>(
       v, nd.ev_pos, nd.ev_e, J, hpos, N, nu, nd.upd_c, nd.n_upd, s2lo, nd.ev_unit, nd.ev_upd, nd.upd_lo);
@@ -1052,6 +1104,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
     x.N = nd.N; x.J = nd.J; x.n_local = nd.n_local; x.n_units = nd.n_units; x.n_lo = nd.n_lo;
     x.ev_pos = nd.ev_pos; x.ev_e = nd.ev_e; x.ev_inv = nd.ev_inv; x.ev_act = nd.ev_act; x.ev_unit = nd.ev_unit;
     x.ev_upd = nd.ev_upd; x.inv_s = nd.inv_s; x.lidf = nd.lidf; x.nxt = nd.nxt; x.u_of = nd.u_of;
+    x.prv = nd.prv; x.upu = nd.upu;
     x.urec = static_cast<const UnitRec*>(nd.urec); x.lid2gid = nd.lid2gid; x.upd_c = nd.upd_c; x.upd_lo = nd.upd_lo;
     hn[w] = x;
   }
@@ -1072,7 +1125,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   ReplayArgs a{};
   uint64_t off = 0;
   a.o_res = off; off += al(max_local * 4 + 16);
-  a.o_runit = off; off += al(max_local * 4 + 16);
+  a.o_nres = off; off += al(n2N * 32768 * 4);
   a.o_bits = off; off += al(n2N * 32768 * 4);
   a.o_c1 = off; off += al(n2N * 1024 * 4);
   a.o_dbits = off; off += al(n2L * 32768 * 4);
@@ -1082,6 +1135,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   a.o_list1 = off; off += al(max_units * sizeof(ListRec));
   a.o_kbuf = off; off += al(((uint64_t)cap_max + 1) * 8);
   a.o_vl = off; off += al(((uint64_t)cap_max + 1) * 12);  // victim list + pivot (unit, position) pairs
+  a.o_vu = off; off += al(max_units * 4);
   a.o_ocall = off; off += al(max_lo * 4);
   a.cta_bytes = off;
   // dynamic shared memory (one CTA per SM):

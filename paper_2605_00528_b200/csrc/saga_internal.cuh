@@ -120,6 +120,8 @@ struct NodeDev {
   uint32_t* ev_unit = nullptr; // [J+1] first unit of event j
   uint32_t* ev_upd = nullptr;  // [J] end of the session-update list for event j
   uint32_t* u_of = nullptr;    // [N] unit of position p | KIND_MIG
+  uint32_t* prv = nullptr;     // [N] previous position of the block at p (NONE at a first touch)
+  uint32_t* upu = nullptr;     // [N] unit of prv[p]
   void* urec = nullptr;        // [n_units] UnitRec (k_replay.cu): t, position range, local owner
   uint32_t n_lo = 0;           // private owners (sessions) with blocks at this node
   uint32_t* upd_lo = nullptr;  // [n_upd] local owner id of each session-update call
