@@ -78,6 +78,12 @@ __device__ __forceinline__ int64_t warp_min64(int64_t x) {
   return x;
 }
 
+// Per-node queue (lane w owns node w), an exact reformulation of the FIFO with kappa servers:
+//   S  calls in service (the FIFO's first min(len, kappa) entries; every one progresses by
+//      min(r, E) each epoch), kept sorted by a finish threshold F = r + V where V is the node's
+//      virtual time (+E per epoch), so an epoch costs O(1 + completions) instead of O(len);
+//   W  waiting calls (never served) in FIFO order with their full work r.
+// L = sum over the queue of min(r, E) = sum_S min(F - V, E) + LW, with LW = sum_W min(r, E).
 template <bool SS>
 __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -87,12 +93,22 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   const uint32_t NS = v.n_sessions, NC = v.n_calls;
   SessRec* sess = SS ? reinterpret_cast<SessRec*>(smem_raw) : a.sess_g;
   uint8_t* moved = SS ? smem_raw + (size_t)NS * sizeof(SessRec) : a.moved_g;
-  const size_t qoff = SS ? (((size_t)NS * (sizeof(SessRec) + 1) + 15) & ~(size_t)15) : 0;
-  uint32_t* qc = reinterpret_cast<uint32_t*>(smem_raw + qoff) + lane * Q;          // session | STARTED
-  uint32_t* qr = reinterpret_cast<uint32_t*>(smem_raw + qoff) + W * Q + lane * Q;  // remaining work (us)
+  size_t off = SS ? (((size_t)NS * (sizeof(SessRec) + 1) + 15) & ~(size_t)15) : 0;
+  int64_t* sF = reinterpret_cast<int64_t*>(smem_raw + off) + (size_t)lane * K;     // S: finish thresholds
+  off += (size_t)W * K * 8;
+  uint32_t* sS = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * K;   // S: sessions
+  off += (size_t)W * K * 4;
+  uint32_t* wS = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * Q;   // W: sessions (ring)
+  off += (size_t)W * Q * 4;
+  uint32_t* wR = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * Q;   // W: work (us)
   __shared__ int32_t cnt[32][32];                       // sessions with aff = w, !fin, by type
   __shared__ int32_t act_tot[32];
-  __shared__ uint32_t xfer_c[64], xfer_r[64];
+  // call records streamed ahead by TMA bulk copies: chunk j (calls [256 j, 256 j + 256)) lives
+  // in buffer j & 1; chunk j + 1 is requested when chunk j is first touched
+  constexpr uint32_t CH = 256;
+  __shared__ __align__(16) CallRec ring[2][CH];
+  __shared__ __align__(8) uint64_t rbar[2];
+  __shared__ uint32_t xfer_s[64], xfer_r[64];
   __shared__ uint32_t xfer_n, n_mig, n_act, errf;
   __shared__ unsigned long long steals, reroutes;
   for (int i = lane; i < 32 * 32; i += 32) (&cnt[0][0])[i] = 0;
@@ -102,10 +118,37 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     for (uint32_t i = lane; i < NS; i += 32) { sess[i] = init; moved[i] = 0; }
   }
   if (lane == 0) { n_mig = 0; n_act = 0; errf = 0; steals = 0; reroutes = 0; xfer_n = 0; }
+  const uint32_t n_chunks = (NC + CH - 1) / CH;
+  auto fetch = [&](uint32_t j) {  // lane 0
+    const uint32_t n = min(CH, NC - j * CH);
+    tma_load_1d(&ring[j & 1][0], a.rec + (size_t)j * CH, n * (uint32_t)sizeof(CallRec), &rbar[j & 1]);
+  };
+  if (lane == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    if (n_chunks > 0) fetch(0);
+    if (n_chunks > 1) fetch(1);
+  }
   __syncwarp();
+  uint32_t have = n_chunks > 1 ? 2u : n_chunks;  // chunks requested so far
+  uint32_t ready = 0;                            // chunks known complete
+  // make calls [c0, c0 + 32) readable: wait for their chunks, request the chunk after them
+  auto ensure = [&](uint32_t c0) {
+    const uint32_t jl = min((c0 + 31) / CH, n_chunks ? n_chunks - 1 : 0);
+    // chunk h reuses the buffer of chunk h - 2, free once no call below chunk h - 1 is needed
+    while (have < n_chunks && have <= jl + 1 && have - 2 < c0 / CH) {
+      if (lane == 0) fetch(have);
+      ++have;
+    }
+    __syncwarp();
+    while (ready <= jl && ready < n_chunks) {
+      mbar_wait(&rbar[ready & 1], (ready >> 1) & 1u);
+      ++ready;
+    }
+  };
   const bool act_lane = lane < W;
-  uint32_t len = 0;
-  int64_t L = 0, idle = 0;
+  uint32_t nS = 0, nW = 0, wh = 0;  // |S|, |W|, ring head
+  int64_t V = 0, LW = 0, L = 0, idle = 0;
   uint32_t next = 0;
   uint64_t e = 1;
 
@@ -113,8 +156,9 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   CallRec pre;
   SessRec ps;
   auto load_pre = [&]() {
+    ensure(next);
     const uint32_t c = next + lane;
-    if (c < NC) pre = a.rec[c];
+    if (c < NC) pre = ring[(c / CH) & 1][c % CH];
     else { pre.e = 0xFFFFFFFFu; pre.s = 0; }
   };
   auto load_ps = [&]() {
@@ -123,58 +167,72 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   load_pre();
   load_ps();
 
-  auto recompute_L = [&]() {
-    int64_t s = 0;
-    for (uint32_t i = 0; i < len; ++i) s += min((int64_t)qr[i], E);
-    L = s;
+  auto w_at = [&](uint32_t i) { uint32_t j = wh + i; return j >= Q ? j - Q : j; };
+  // insert a call into S keeping F ascending
+  auto s_insert = [&](uint32_t sid, int64_t F) {
+    uint32_t i = nS;
+    while (i > 0 && sF[i - 1] > F) { sF[i] = sF[i - 1]; sS[i] = sS[i - 1]; --i; }
+    sF[i] = F; sS[i] = sid; ++nS;
   };
-  // oldest pending (never served) call of a session that is not `moved` and has no call in
-  // service in this queue (DESIGN.md R-steal)
+  // move waiting calls into service while a server is free (FIFO order)
+  auto admit = [&]() {
+    while (nS < K && nW > 0) {
+      const uint32_t j = w_at(0);
+      const int64_t r = wR[j];
+      LW -= min(r, E);
+      s_insert(wS[j], V + r);
+      wh = w_at(1); --nW;
+    }
+  };
+  // drop the calls of S whose threshold is reached (a prefix); returns the work they had left
+  auto complete = [&](int64_t Vnew, int64_t Vold, int64_t& served) -> uint32_t {
+    uint32_t m = 0;
+    while (m < nS && sF[m] <= Vnew) { served += sF[m] - Vold; moved[sS[m]] = 0; ++m; }
+    if (m) {
+      for (uint32_t i = m; i < nS; ++i) { sF[i - m] = sF[i]; sS[i - m] = sS[i]; }
+      nS -= m;
+    }
+    return m;
+  };
+  auto load_of = [&]() {
+    int64_t l = LW;
+    uint32_t i = 0;
+    for (; i < nS && sF[i] - V < E; ++i) l += sF[i] - V;
+    l += (int64_t)(nS - i) * E;
+    return l;
+  };
+  // oldest waiting call of a session that is not `moved` and has no call in service here
   auto find_stealable = [&]() -> int32_t {
-    for (uint32_t i = 0; i < len; ++i) {
-      uint32_t x = qc[i];
-      if (x & STARTED) continue;
-      uint32_t s = x & CMASK;
+    for (uint32_t i = 0; i < nW; ++i) {
+      const uint32_t s = wS[w_at(i)];
       if (moved[s]) continue;
       bool busy = false;
-      for (uint32_t j = 0; j < len; ++j)
-        if ((qc[j] & STARTED) && (qc[j] & CMASK) == s) { busy = true; break; }
+      for (uint32_t j = 0; j < nS; ++j) if (sS[j] == s) { busy = true; break; }
       if (!busy) return (int32_t)s;
     }
     return -1;
   };
 
   while (true) {
-    bool any = __ballot_sync(0xffffffffu, act_lane && len > 0) != 0;
+    const bool any = __ballot_sync(0xffffffffu, act_lane && (nS + nW) > 0) != 0;
     if (next >= NC && !any) break;
     const int64_t Te = (int64_t)e * E;
     bool got = false;
     // ---------------- P1 service: the first kappa calls progress by one epoch ----------------
     if (act_lane) {
-      int64_t served = 0, Ls = 0;
-      uint32_t k = 0;
-      for (uint32_t i = 0; i < len; ++i) {
-        uint32_t x = qc[i], r = qr[i];
-        if (i < K) {
-          uint32_t d = (uint32_t)min((int64_t)r, E);
-          r -= d;
-          served += d;
-          x |= STARTED;
-          if (r == 0) { moved[x & CMASK] = 0; continue; }
-        }
-        qc[k] = x; qr[k] = r; ++k;
-        Ls += min((int64_t)r, E);
-      }
-      len = k;
+      admit();
+      int64_t served = 0;
+      const uint32_t m = complete(V + E, V, served);
+      served += (int64_t)nS * E;  // every remaining call in service progressed by E
+      (void)m;
+      V += E;
       idle = served == 0 ? idle + 1 : 0;
-      L = Ls;
+      L = load_of();
     }
     __syncwarp();
     // ---------------- P2 steal: idle thief AND load-ratio guard (P:361, P:766(a)) ----------------
     uint32_t thieves = __ballot_sync(0xffffffffu, act_lane && idle * E >= a.t_idle_us);
-    bool unst = false;
-    if (act_lane) for (uint32_t i = 0; i < len; ++i) if (!(qc[i] & STARTED)) { unst = true; break; }
-    if (thieves && __ballot_sync(0xffffffffu, unst)) {
+    if (thieves && __ballot_sync(0xffffffffu, act_lane && nW > 0)) {
       bool stole = false;
       while (thieves) {
         const uint32_t th = __ffs(thieves) - 1;
@@ -186,30 +244,37 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
         if (!O) continue;
         uint64_t r = splitmix64(a.seed ^ (e * PHI) ^ (uint64_t)th) % (uint64_t)__popc(O);
         uint32_t vv = 0, cntb = 0;
-        for (uint32_t m = O; m; m &= m - 1) { if (cntb == r) { vv = __ffs(m) - 1; break; } ++cntb; }
+        for (uint32_t mm = O; mm; mm &= mm - 1) { if (cntb == r) { vv = __ffs(mm) - 1; break; } ++cntb; }
         const int32_t s = __shfl_sync(0xffffffffu, cand, vv);
-        if (lane == vv) {
-          uint32_t k = 0, m = 0;
-          for (uint32_t i = 0; i < len; ++i) {
-            uint32_t x = qc[i];
-            if ((x & CMASK) == (uint32_t)s) {
-              if (m < 64) { xfer_c[m] = x; xfer_r[m] = qr[i]; }
+        if (lane == vv) {  // every call of s here is waiting: move them, order kept
+          uint32_t kk = 0, m = 0;
+          for (uint32_t i = 0; i < nW; ++i) {
+            const uint32_t j = w_at(i);
+            const uint32_t x = wS[j], rr = wR[j];
+            if (x == (uint32_t)s) {
+              if (m < 64) { xfer_s[m] = x; xfer_r[m] = rr; }
               ++m;
-            } else { qc[k] = x; qr[k] = qr[i]; ++k; }
+              LW -= min((int64_t)rr, E);
+            } else {
+              const uint32_t jd = w_at(kk);
+              wS[jd] = x; wR[jd] = rr; ++kk;
+            }
           }
           if (m > 64) atomicOr(&errf, 4u);
-          len = k;
+          nW = kk;
           xfer_n = m;
-          recompute_L();
+          L = load_of();
         }
         __syncwarp();
         if (lane == th) {
-          uint32_t m = min(xfer_n, 64u);
+          const uint32_t m = min(xfer_n, 64u);
           for (uint32_t i = 0; i < m; ++i) {
-            if (len >= Q) { atomicOr(&errf, 1u); break; }
-            qc[len] = xfer_c[i]; qr[len] = xfer_r[i]; ++len;
+            if (nW >= Q) { atomicOr(&errf, 1u); break; }
+            const uint32_t j = w_at(nW);
+            wS[j] = xfer_s[i]; wR[j] = xfer_r[i]; ++nW;
+            LW += min((int64_t)xfer_r[i], E);
           }
-          recompute_L();
+          L = load_of();
           idle = 0;
           got = true;
         }
@@ -274,8 +339,13 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
         const bool fin_old = __shfl_sync(0xffffffffu, fin, i);
         const bool f_new = __shfl_sync(0xffffffffu, f_new_l, i);
         if (lane == w) {
-          if (len >= Q) atomicOr(&errf, 1u);
-          else { qc[len] = si; qr[len] = omega; ++len; L += min((int64_t)omega, E); }
+          if (nW >= Q) atomicOr(&errf, 1u);
+          else {
+            const uint32_t j = w_at(nW);
+            wS[j] = si; wR[j] = omega; ++nW;
+            LW += min((int64_t)omega, E);
+            L += min((int64_t)omega, E);
+          }
           got = true;
         }
         if (lane == 0) {
@@ -323,41 +393,39 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     }
     if (errf & 1u) break;
     // ---------------- closed-form advance over service-only epochs ----------------
-    const bool all_fit = __ballot_sync(0xffffffffu, act_lane && len > K) == 0;
+    const bool all_fit = __ballot_sync(0xffffffffu, act_lane && nS + nW > K) == 0;
     if (all_fit) {
       const uint32_t e_next = __shfl_sync(0xffffffffu, pre.e, 0);
+      if (act_lane) admit();  // everything fits: every queued call is served each epoch
       uint64_t k;
       if (next >= NC) {
-        int64_t mx = 0;
-        if (act_lane) for (uint32_t i = 0; i < len; ++i) mx = max(mx, (int64_t)qr[i]);
+        int64_t mx = (act_lane && nS) ? sF[nS - 1] - V : 0;
         mx = -warp_min64(-mx);
         k = (uint64_t)ceil_div64(mx, E);
       } else {
         k = (uint64_t)e_next - 1 - e;
       }
       if (k > 0 && act_lane) {
-        const int64_t budget = (int64_t)k * E;
-        int64_t mx = 0, Ls = 0;
-        uint32_t kk = 0;
-        for (uint32_t i = 0; i < len; ++i) {
-          int64_t r = qr[i];
-          mx = max(mx, r);
-          if (r <= budget) { moved[qc[i] & CMASK] = 0; continue; }
-          qc[kk] = qc[i] | STARTED; qr[kk] = (uint32_t)(r - budget); ++kk;
-          Ls += min(r - budget, E);
-        }
-        if (len == 0) idle += (int64_t)k;
+        const int64_t mx = nS ? sF[nS - 1] - V : 0;
+        const bool empty = nS + nW == 0;
+        int64_t served = 0;
+        complete(V + (int64_t)k * E, V, served);
+        if (empty) idle += (int64_t)k;
         else {
-          uint64_t m = (uint64_t)ceil_div64(mx, E);
+          const uint64_t m = (uint64_t)ceil_div64(mx, E);
           idle = m >= k ? 0 : (int64_t)(k - m);
         }
-        len = kk;
-        L = Ls;
+        V += (int64_t)k * E;
+        L = load_of();
       }
       e += k;
     }
     __syncwarp();
     ++e;
+  }
+  while (ready < have) {  // no bulk copy may still target this CTA's shared memory at exit
+    mbar_wait(&rbar[ready & 1], (ready >> 1) & 1u);
+    ++ready;
   }
   if (lane == 0) {
     a.out_n[0] = n_mig;
@@ -388,12 +456,16 @@ saga_status run_placement(saga_trace* t) {
   const TraceView& v = t->v;
   const uint32_t W = v.n_nodes;
   const size_t max_smem = 200 * 1024;
+  const uint32_t K = t->pcfg.kappa;
+  if (K > 256) { set_error("saga_load_trace: kappa > 256 is not supported"); return SAGA_ERR_INVALID_ARG; }
   const size_t sess_bytes = ((size_t)v.n_sessions * (sizeof(SessRec) + 1) + 15) & ~(size_t)15;
-  // sessions in shared memory if that still leaves >= 256 queue slots per node
-  const bool ss = sess_bytes + 256ull * 8 * W <= max_smem;
-  uint32_t qcap = (uint32_t)((max_smem - (ss ? sess_bytes : 0)) / (8ull * W));
+  const size_t srv_bytes = (size_t)W * K * 12;  // S: finish thresholds + sessions
+  // sessions in shared memory if that still leaves >= 256 waiting slots per node
+  const bool ss = sess_bytes + srv_bytes + 256ull * 8 * W <= max_smem;
+  if (srv_bytes + 64ull * 8 * W > max_smem) { set_error("saga_load_trace: kappa x nodes too large"); return SAGA_ERR_INVALID_ARG; }
+  uint32_t qcap = (uint32_t)((max_smem - (ss ? sess_bytes : 0) - srv_bytes) / (8ull * W));
   if (qcap > 65536) qcap = 65536;
-  const size_t smem = (ss ? sess_bytes : 0) + size_t(qcap) * W * 8;
+  const size_t smem = (ss ? sess_bytes : 0) + srv_bytes + size_t(qcap) * W * 8;
   uint32_t mig_cap = v.n_calls + v.n_sessions + 64;
   uint32_t act_cap = v.n_calls + mig_cap + 64;
   t->node_of = dalloc<uint8_t>(t, v.n_calls);
