@@ -9,7 +9,14 @@ A2 placement, A3 streams) -> saga_belady_next_use per owned node (A4) -> W_lo/W_
 per second, max over ranks, inputs resident in HBM; e2e = the same through the public API from
 pinned host buffers with the H2D copy of the trace and the D2H read of the counters timed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+At N > 1 GPUs the default is `--shard trials`: rank r replays its own seeded trial of the workload
+(seed = the config's seed + 1000 r; rank 0 is the canonical trace) -- independent problems, so the
+per-GPU work is fixed (weak scaling) -- and the per-trial counter tensors are summed over ranks by
+the NCCL all-reduce of A8 every step (the paper averages over seeds).  `--shard nodes` instead
+splits ONE trace by cache node (w mod R) with the W_lo/W_hi max-all-reduce and the counter
+sum-all-reduce (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--shard trials|nodes] [--impl reference]
 """
 from __future__ import annotations
 
@@ -184,6 +191,7 @@ def main():
     ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -202,12 +210,20 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
-    desc = make(args.config, n_sessions=args.n_sessions)
+    shard = args.shard or ("trials" if world > 1 else "nodes")
+    trials = shard == "trials"
+    seed = None
+    if trials and rank > 0 and args.config != "C1":
+        import inspect
+        from gen import CONFIGS
+        seed = inspect.signature(CONFIGS[args.config]).parameters["seed"].default + 1000 * rank
+    desc = make(args.config, n_sessions=args.n_sessions, seed=seed)
     pc = place_cfg_for(desc)
     rcfg = dict(policy_mask=3)
     caps_fn = sweep_for(args.config)
-    shard_caps = desc.n_nodes == 1 and world > 1
+    shard_caps = (not trials) and desc.n_nodes == 1 and world > 1
     comm = saga.Comm(rank, world, local) if world > 1 else None
+    p_rank, p_world, p_comm = (0, 1, None) if trials else (rank, world, comm)
     stream = torch.cuda.Stream(device=dev)
     host_pinned = saga.HostDesc(desc, pinned=True)
     # device-resident descriptor for `value` (the library deep-copies it device-to-device)
@@ -230,8 +246,11 @@ def main():
     def step(host):
         nonlocal counters
         with torch.cuda.stream(stream):
-            t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=rank, world=world, comm=comm, device=local,
-                                             stream=stream, host=host, counters=counters, shard_caps=shard_caps)
+            t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=p_rank, world=p_world, comm=p_comm,
+                                             device=local, stream=stream, host=host, counters=counters,
+                                             shard_caps=shard_caps)
+            if trials and comm is not None:  # A8: combine the per-trial counters over ranks
+                comm.allreduce(ctr, op=0, stream=t.stream)
         counters = ctr
         return t, caps, ctr
 
@@ -247,7 +266,8 @@ def main():
     # per-step work (access-replays over all ranks)
     t, caps, ctr = step(dd)
     stream.synchronize()
-    mine = pipeline.owned_nodes(desc.n_nodes, rank, world) if not shard_caps else [0]
+    mine = (list(range(desc.n_nodes)) if trials else pipeline.owned_nodes(desc.n_nodes, rank, world)) \
+        if not shard_caps else [0]
     n_acc_local = sum(t.info(w)[0] for w in mine)
     n_pol = 2
     if shard_caps:
@@ -330,7 +350,7 @@ def main():
             continue
         ms_k = pm[i] / args.steps
         byt = algorithmic_bytes(nm, n_access / max(world, 1) if not shard_caps else n_access,
-                                replay_accesses / max(world, 1), desc.n_calls, key_bits)
+                                replay_accesses / max(world, 1), desc.n_calls, key_bits)  # per rank
         kernels[nm] = {"ms_per_step": ms_k, "launches_per_step": pn[i] / args.steps, "share": ms_k / ms,
                        "algorithmic_gb_s": (byt / (ms_k / 1e3) / 1e9) if byt and ms_k > 0 else None}
     dom = max((k for k in kernels if k in ("sort", "segscan", "epoch_stats", "replay", "expand")),
@@ -356,14 +376,16 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if trials and world > 1 else "strong",
+            "vs_baseline": None,
             "dtype": "int64/fp32", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "trace": desc.name,
                        "nodes": desc.n_nodes, "caps": caps, "policies": ["AEG", "BELADY"],
                        "trace_accesses": n_access, "access_replays_per_step": replay_accesses,
                        "trace_accesses_per_s": n_access / (ms / 1e3),
                        "l2": "inputs larger than L2 (node streams 4 B/access + per-node next-use arrays)",
-                       "sharding": "capacity points" if shard_caps else "cache nodes w mod R"},
+                       "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
+                                    else ("capacity points" if shard_caps else "cache nodes w mod R"))},
             "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels,
             "counters_checksum": int(np.bitwise_xor.reduce(counters_host.reshape(-1).view(np.uint64))),

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     }
   };
   const bool act_lane = lane < W;
-  uint32_t nS = 0, nW = 0, wh = 0;  // |S|, |W|, ring head
+  uint32_t nS = 0, nW = 0, wh = 0, sh = 0;  // |S|, |W|, ring heads of W and S (S is a ring of K)
   int64_t V = 0, LW = 0, L = 0, idle = 0;
   uint32_t next = 0;
   uint64_t e = 1;
@@ -168,11 +168,19 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   load_ps();
 
   auto w_at = [&](uint32_t i) { uint32_t j = wh + i; return j >= Q ? j - Q : j; };
-  // insert a call into S keeping F ascending
+  auto s_at = [&](uint32_t i) { uint32_t j = sh + i; return j >= K ? j - K : j; };
+  // insert a call into S keeping F ascending (new calls usually land at the tail)
   auto s_insert = [&](uint32_t sid, int64_t F) {
     uint32_t i = nS;
-    while (i > 0 && sF[i - 1] > F) { sF[i] = sF[i - 1]; sS[i] = sS[i - 1]; --i; }
-    sF[i] = F; sS[i] = sid; ++nS;
+    while (i > 0) {
+      const uint32_t jp = s_at(i - 1);
+      if (sF[jp] <= F) break;
+      const uint32_t j = s_at(i);
+      sF[j] = sF[jp]; sS[j] = sS[jp];
+      --i;
+    }
+    const uint32_t j = s_at(i);
+    sF[j] = F; sS[j] = sid; ++nS;
   };
   // move waiting calls into service while a server is free (FIFO order)
   auto admit = [&]() {
@@ -187,17 +195,23 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   // drop the calls of S whose threshold is reached (a prefix); returns the work they had left
   auto complete = [&](int64_t Vnew, int64_t Vold, int64_t& served) -> uint32_t {
     uint32_t m = 0;
-    while (m < nS && sF[m] <= Vnew) { served += sF[m] - Vold; moved[sS[m]] = 0; ++m; }
-    if (m) {
-      for (uint32_t i = m; i < nS; ++i) { sF[i - m] = sF[i]; sS[i - m] = sS[i]; }
-      nS -= m;
+    while (m < nS) {
+      const uint32_t j = s_at(0);
+      if (sF[j] > Vnew) break;
+      served += sF[j] - Vold;
+      moved[sS[j]] = 0;
+      sh = s_at(1); --nS; ++m;
     }
     return m;
   };
   auto load_of = [&]() {
     int64_t l = LW;
     uint32_t i = 0;
-    for (; i < nS && sF[i] - V < E; ++i) l += sF[i] - V;
+    for (; i < nS; ++i) {
+      const int64_t r = sF[s_at(i)] - V;
+      if (r >= E) break;
+      l += r;
+    }
     l += (int64_t)(nS - i) * E;
     return l;
   };
@@ -207,7 +221,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
       const uint32_t s = wS[w_at(i)];
       if (moved[s]) continue;
       bool busy = false;
-      for (uint32_t j = 0; j < nS; ++j) if (sS[j] == s) { busy = true; break; }
+      for (uint32_t j = 0; j < nS; ++j) if (sS[s_at(j)] == s) { busy = true; break; }
       if (!busy) return (int32_t)s;
     }
     return -1;
@@ -399,20 +413,21 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
       if (act_lane) admit();  // everything fits: every queued call is served each epoch
       uint64_t k;
       if (next >= NC) {
-        int64_t mx = (act_lane && nS) ? sF[nS - 1] - V : 0;
+        int64_t mx = (act_lane && nS) ? sF[s_at(nS - 1)] - V : 0;
         mx = -warp_min64(-mx);
         k = (uint64_t)ceil_div64(mx, E);
       } else {
         k = (uint64_t)e_next - 1 - e;
       }
       if (k > 0 && act_lane) {
-        const int64_t mx = nS ? sF[nS - 1] - V : 0;
+        const int64_t mx = nS ? sF[s_at(nS - 1)] - V : 0;  // < 2^32 (work is u32 us)
         const bool empty = nS + nW == 0;
         int64_t served = 0;
         complete(V + (int64_t)k * E, V, served);
         if (empty) idle += (int64_t)k;
         else {
-          const uint64_t m = (uint64_t)ceil_div64(mx, E);
+          const uint32_t mx32 = (uint32_t)mx, E32 = (uint32_t)E;
+          const uint64_t m = mx32 / E32 + (mx32 % E32 != 0u);
           idle = m >= k ? 0 : (int64_t)(k - m);
         }
         V += (int64_t)k * E;

@@ -192,8 +192,9 @@ saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* c
   g_err.clear();
   if (!desc || !cfg || !out) { set_error("saga_load_trace: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   *out = nullptr;
-  if (cfg->epoch_us <= 0 || cfg->kappa == 0 || cfg->prefill_tok_s == 0 || cfg->decode_tok_s == 0) {
-    set_error("saga_load_trace: epoch_us, kappa, prefill_tok_s and decode_tok_s must be positive");
+  if (cfg->epoch_us <= 0 || cfg->epoch_us > 1000000000ll || cfg->kappa == 0 || cfg->prefill_tok_s == 0 ||
+      cfg->decode_tok_s == 0) {
+    set_error("saga_load_trace: epoch_us must be in (0, 1e9] and kappa, prefill_tok_s, decode_tok_s positive");
     return SAGA_ERR_INVALID_ARG;
   }
   int ndev = 0;
