@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   // drop the calls of S whose threshold is reached (a prefix); returns the work they had left
   auto complete = [&](int64_t Vnew, int64_t Vold, int64_t& served) -> uint32_t {
     uint32_t m = 0;
-    while (m < nS) {
+    while (nS > 0) {
       const uint32_t j = s_at(0);
       if (sF[j] > Vnew) break;
       served += sF[j] - Vold;
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
         complete(V + (int64_t)k * E, V, served);
         if (empty) idle += (int64_t)k;
         else {
-          const uint32_t mx32 = (uint32_t)mx, E32 = (uint32_t)E;
+          const uint32_t mx32 = (uint32_t)mx, E32 = (uint32_t)E;  // 0 <= mx < 2^32
           const uint64_t m = mx32 / E32 + (mx32 % E32 != 0u);
           idle = m >= k ? 0 : (int64_t)(k - m);
         }
