@@ -125,6 +125,62 @@ def algorithmic_bytes(cat, n_access, n_replay_access, n_calls, key_bits):
     }.get(cat, 0)
 
 
+def bulk_score_select(t, desc, stream, dev, reps=5, n_seg=1024, seg_len=32768, k_frac=0.01):
+    """A5 / A6 in bulk on a C5-shaped snapshot -- n_seg segments of seg_len
+    candidates (runs of consecutive local ids, i.e. runs of one session's blocks), inputs >> L2,
+    k = 1 % per segment.  Returns per-kernel ms and algorithmic GB/s:
+    AEG score 24 B/candidate (lid 4 + t_last 8 + owner 4 -> key 8), BELADY key 16 B (lid 4 + nu 4
+    -> key 8), select 8 B/candidate (+ 4 B per victim written)."""
+    import torch
+    from paper_2605_00528_b200 import saga
+    nl = t.info(0)[1]
+    if nl < seg_len + 1:
+        return None
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    n = n_seg * seg_len
+    starts = torch.randint(0, nl - seg_len, (n_seg, 1), generator=g, device=dev, dtype=torch.int64)
+    lid = (starts + torch.arange(seg_len, device=dev, dtype=torch.int64)).reshape(-1).to(torch.int32)
+    e_last = int(desc.call_t_us.max()) // 100_000 + 1
+    Te = e_last * 100_000
+    t_last = Te - torch.randint(0, 60_000_000, (n,), generator=g, device=dev, dtype=torch.int64)
+    nu = torch.randint(0, 2 ** 31, (n,), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
+    i32 = lambda x: torch.full((n_seg,), x, dtype=torch.int32, device=dev)
+    off = torch.arange(0, n + 1, seg_len, dtype=torch.int64, device=dev)
+    batch = dict(seg_node=i32(0), seg_epoch=i32(e_last), seg_occ=i32(seg_len), seg_cap=i32(seg_len), seg_act=i32(1),
+                 seg_off=off, cand_lid=lid, cand_t_last=t_last, cand_nu=nu)
+    key = torch.empty(n, dtype=torch.int64, device=dev)
+    kk = max(1, int(seg_len * k_frac))
+    kreq = torch.full((n_seg,), kk, dtype=torch.int32, device=dev)
+    oo = torch.arange(0, n_seg * kk + 1, kk, dtype=torch.int64, device=dev)
+    vic = torch.empty(n_seg * kk, dtype=torch.int32, device=dev)
+    out = {}
+
+    def timed(fn):
+        with torch.cuda.stream(stream):
+            fn()
+            stream.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    ms = timed(lambda: t.aeg_score(batch, {}, key, None, policy=saga.POLICY_AEG))
+    out["score_aeg"] = {"ms": ms, "bytes_per_candidate": 24, "algorithmic_gb_s": n * 24 / (ms / 1e3) / 1e9}
+    ms = timed(lambda: t.aeg_score(batch, {}, key, None, policy=saga.POLICY_BELADY))
+    out["score_belady"] = {"ms": ms, "bytes_per_candidate": 16, "algorithmic_gb_s": n * 16 / (ms / 1e3) / 1e9}
+    t.aeg_score(batch, {}, key, None, policy=saga.POLICY_AEG)
+    ms = timed(lambda: saga.evict_select(key, off, kreq, oo, vic, stream=stream))
+    out["select"] = {"ms": ms, "bytes_per_candidate": 8,
+                     "algorithmic_gb_s": (n * 8 + n_seg * kk * 4) / (ms / 1e3) / 1e9}
+    out["snapshot"] = f"{n_seg} segments x {seg_len} candidates (runs of consecutive local ids), k = {kk}"
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (oracle/), as it stands, on a bounded sample of the workload."""
     rank = int(os.environ.get("RANK", "0"))
@@ -191,6 +247,7 @@ def main():
     ap.add_argument("--impl", default="saga", choices=["saga", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bulk", action="store_true")
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
     args = ap.parse_args()
     if args.impl == "reference":
@@ -369,6 +426,16 @@ def main():
                 "traffic": traffic, "peak_source": peak_kind,
                 "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
 
+    bulk = None
+    if rank == 0 and not args.no_bulk:
+        t_b, _, _ = step(dd)
+        stream.synchronize()
+        bulk = bulk_score_select(t_b, desc, stream, dev)
+        t_b.free()
+        if bulk:
+            for kname, kv in bulk.items():
+                if isinstance(kv, dict):
+                    kv["frac"] = kv["algorithmic_gb_s"] / peak
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(desc, pc, caps, os.cpu_count() or 1)
@@ -387,7 +454,7 @@ def main():
                        "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
                                     else ("capacity points" if shard_caps else "cache nodes w mod R"))},
             "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels,
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels, "bulk_score_select": bulk,
             "counters_checksum": int(np.bitwise_xor.reduce(counters_host.reshape(-1).view(np.uint64))),
         }
         print(json.dumps(line), flush=True)

@@ -134,7 +134,14 @@ struct Smem {
   uint32_t n_app, n_piv, n_vict, n_vu;
   uint32_t ilo, ihi;
   uint32_t tot_dead, tot_pend;  // BELADY: set bits of the two hierarchical bitmaps
+  __align__(8) uint64_t pbar[2];  // TMA prefetch stages of per-position arrays
 };
+
+// Per-position arrays of an epoch (lidf, u_of, nxt, prv, upu) are staged in shared memory by TMA
+// bulk copies one epoch ahead: PF positions per array and stage, two stages.
+constexpr uint32_t PF = 2048;
+constexpr uint32_t NPA = 5;
+constexpr uint32_t PF_WORDS = 2 * NPA * PF;
 
 // first failed invariant of the launch: [0] = line, [1..3] = values (host reports it)
 __device__ __forceinline__ void dbg_fail(uint32_t* dbg, uint32_t line, uint32_t x, uint32_t y, uint32_t z) {
@@ -191,16 +198,37 @@ __device__ __forceinline__ void hb_clear(const HB& h, uint32_t i) {
   atomicSub(&h.c1[i >> 10], 1u);
   atomicSub(&h.c2[i >> 20], 1u);
 }
-// warp-cooperative update (all lanes call): lanes with `act` set (or clear) bit i; the count
-// updates of lanes that hit the same 1024-bit block are aggregated.
-__device__ __forceinline__ void hb_update_warp(const HB& h, bool act, uint32_t i, bool set) {
+// Warp-collective (all lanes call): lanes with `act` set (or clear) bit `idx` of `bits`; one
+// atomic per distinct word (lanes usually hit few words: positions and local ids come in runs).
+__device__ __forceinline__ void warp_bits(uint32_t* bits, bool act, uint32_t idx, bool set) {
   const uint32_t am = __ballot_sync(0xffffffffu, act);
   if (!act) return;
-  const int lane = threadIdx.x & 31;
-  if (set) atomicOr(&h.bits[i >> 5], 1u << (i & 31));
-  else atomicAnd(&h.bits[i >> 5], ~(1u << (i & 31)));
+  const uint32_t w = idx >> 5;
+  const uint32_t peers = __match_any_sync(am, w);
+  const uint32_t m = __reduce_or_sync(peers, 1u << (idx & 31));
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+    if (set) atomicOr(&bits[w], m);
+    else atomicAnd(&bits[w], ~m);
+  }
+}
+// Warp-collective: lanes with `act` add (or subtract) 1 to counts[key]; one atomic per distinct key.
+__device__ __forceinline__ void warp_count(uint32_t* counts, bool act, uint32_t key, bool add) {
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  if (!act) return;
+  const uint32_t peers = __match_any_sync(am, key);
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+    const uint32_t n = __popc(peers);
+    atomicAdd(&counts[key], add ? n : (uint32_t)(-(int32_t)n));
+  }
+}
+// warp-collective update of a hierarchical bitmap: bits, then the c1 / c2 counts
+__device__ __forceinline__ void hb_update_warp(const HB& h, bool act, uint32_t i, bool set) {
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  if (!am) return;
+  warp_bits(h.bits, act, i, set);
+  if (!act) return;
   const uint32_t p1 = __match_any_sync(am, i >> 10);
-  if (lane == 31 - __clz(p1)) {
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(p1) - 1)) {
     const uint32_t n = __popc(p1);
     atomicAdd(&h.c1[i >> 10], set ? n : (uint32_t)(-(int32_t)n));
     atomicAdd(&h.c2[i >> 20], set ? n : (uint32_t)(-(int32_t)n));
@@ -382,7 +410,7 @@ __device__ __forceinline__ uint32_t owner_size(const TraceView& v, const CallKey
   } while (0)
 
 constexpr uint32_t VT_LID = 0x80000000u;  // victim-list tag: the entry is a local id, else a position
-constexpr int UNR = 4;                    // record chunks whose loads are issued together (R2 / R4)
+constexpr int UNR = 2;                    // record chunks whose loads are issued together (R2 / R4)
 
 __device__ __forceinline__ uint32_t unit_mask(uint32_t wi, uint32_t pa, uint32_t pe) {
   uint32_t m = 0xffffffffu;
@@ -394,8 +422,12 @@ __device__ __forceinline__ uint32_t unit_mask(uint32_t wi, uint32_t pa, uint32_t
 __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
   __shared__ Smem sm;
   __shared__ long long s_ctr[SAGA_NCOUNT];
-  extern __shared__ __align__(16) uint32_t dyn[];
+  extern __shared__ __align__(16) uint32_t dyn_all[];
+  uint32_t* const dyn = dyn_all + PF_WORDS;  // per-item count / table region (after the staging area)
   Par par;
+  if (threadIdx.x == 0) { mbar_init(&sm.pbar[0], 1); mbar_init(&sm.pbar[1], 1); }
+  __syncthreads();
+  uint32_t pf_seq = 0;  // prefetches issued by this CTA (uniform); stage = seq & 1, parity = (seq >> 1) & 1
   const TraceView& v = a.v;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* base = a.scratch + (uint64_t)blockIdx.x * a.cta_bytes;
@@ -472,6 +504,32 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
     unsigned long long hash = 0;
     uint32_t bad = 0;
     long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_t = clock64();
+    const uint32_t npa = belady ? 3u : NPA;       // BELADY never reads prv / upu
+    const uint32_t* pa_src[NPA] = {nd.lidf, nd.u_of, nd.nxt, nd.prv, nd.upu};
+    // staged epoch: event pf_j in stage pf_seq & 1, covering positions [pf_b0, pf_b0 + pf_n)
+    uint32_t pf_j = NONE, pf_n = 0;
+    uint64_t pf_b0 = 0;
+    auto issue = [&](uint32_t jj) {  // uniform; thread 0 issues the bulk copies of event jj
+      const uint64_t q0 = nd.ev_pos[jj], q1 = nd.ev_pos[jj + 1];
+      pf_j = jj;
+      pf_b0 = q0 & ~3ull;
+      pf_n = (uint32_t)min((unsigned long long)(((q1 - pf_b0) + 3) & ~3ull), (unsigned long long)PF);
+      if (threadIdx.x == 0) {
+        const uint32_t st = pf_seq & 1u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.pbar[st])),
+                     "r"(pf_n * 4u * npa) : "memory");
+        for (uint32_t k2 = 0; k2 < npa; ++k2)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(smem_u32(dyn_all + (st * NPA + k2) * PF)), "l"(pa_src[k2] + pf_b0), "r"(pf_n * 4u),
+                       "r"(smem_u32(&sm.pbar[st])) : "memory");
+      }
+      ++pf_seq;
+    };
+    auto await_pf = [&]() {  // all threads: the staged epoch has landed
+      const uint32_t sq = pf_seq - 1u;
+      mbar_wait(&sm.pbar[sq & 1u], (sq >> 1) & 1u);
+    };
 
     for (uint32_t j = 0; j < nd.J; ++j) {
       const uint32_t e = nd.ev_e[j];
@@ -518,6 +576,22 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       if (P0 == P1) continue;    // only empty record groups (the oracle skips the epoch)
       __syncthreads();
       if (threadIdx.x == 0) sm.n_vict = 0;
+      // staged per-position arrays of this epoch (issued one epoch ahead), then stage the next one
+      if (pf_j != j) {
+        if (pf_j != NONE) await_pf();  // drain a stale stage before reusing the sequence
+        issue(j);
+      }
+      await_pf();
+      const uint32_t* stg = dyn_all + ((pf_seq - 1u) & 1u) * NPA * PF;
+      const uint64_t sb0 = pf_b0;
+      const uint32_t sn = pf_n;
+      // (the other stage was last read two epochs ago, before this epoch's first barrier)
+      if (j + 2 < nd.J && nd.ev_pos[j + 2] > nd.ev_pos[j + 1]) issue(j + 1);
+      // position p's value of array k: staged when p - sb0 < sn, else from global memory
+      auto P = [&](uint32_t k2, uint64_t p) -> uint32_t {
+        const uint64_t o = p - sb0;
+        return o < sn ? stg[k2 * PF + o] : pa_src[k2][p];
+      };
       PH(0);
       // ---- R2: |A|, new = |A \ S|; hits / misses; in-flight blocks leave the index ----
       uint32_t nA = 0, nnew = 0;
@@ -533,10 +607,10 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           const uint64_t wbu = wb + (uint64_t)u * RT;
           const uint64_t pb = wbu + lane;
           in[u] = pb >= P0 && pb < P1;
-          lf[u] = in[u] ? nd.lidf[pb] : 0u;
-          uo[u] = in[u] ? nd.u_of[pb] : 0u;
-          pv[u] = (in[u] && !belady) ? nd.prv[pb] : 0u;
-          up[u] = (in[u] && !belady) ? nd.upu[pb] : 0u;
+          lf[u] = in[u] ? P(0, pb) : 0u;
+          uo[u] = in[u] ? P(1, pb) : 0u;
+          pv[u] = (in[u] && !belady) ? P(3, pb) : 0u;
+          up[u] = (in[u] && !belady) ? P(4, pb) : 0u;
           nw[u] = wbu < P1 ? nres[wbu >> 5] : 0u;
         }
 #pragma unroll
@@ -561,9 +635,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             atomicAnd(&nres[wbu >> 5], ~rm);
             if (belady) { atomicSub(&pend.c1[wbu >> 10], (uint32_t)__popc(rm)); atomicSub(&pend.c2[wbu >> 20], (uint32_t)__popc(rm)); }
           }
-          if (!belady && resident) {
-            atomicAnd(&alive[pv[u] >> 5], ~(1u << (pv[u] & 31)));
-            atomicSub(&cnt[up[u]], 1u);
+          if (!belady) {
+            warp_bits(alive, resident, pv[u], false);
+            warp_count(cnt, resident, up[u], false);
           }
         }
       }
@@ -753,15 +827,18 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         // listed victims: positions (block at that position) or local ids (VT_LID)
         const uint32_t nvl = sm.n_vict;
         if (threadIdx.x == 0 && nvl > k) dbg_fail(a.dbg, __LINE__, nvl, k, pol);
-        for (uint32_t i = threadIdx.x; i < nvl; i += RT) {
-          const uint32_t x = vlist[i];
-          const uint32_t lid = (x & VT_LID) ? (x & ~VT_LID) : (nd.lidf[x] & LID_MASK);
+        for (uint32_t i = threadIdx.x; i < ((nvl + 31) & ~31u); i += RT) {
+          const bool in = i < nvl;
+          const uint32_t x = in ? vlist[i] : 0u;
+          const uint32_t lid = (x & VT_LID) ? (x & ~VT_LID) : (in ? nd.lidf[x] & LID_MASK : 0u);
           if (!belady) {  // a victim's next use is no longer resident
-            const uint32_t qn = nd.nxt[x];
-            if (qn != INF32) atomicAnd(&nres_a[qn >> 5], ~(1u << (qn & 31)));
+            const uint32_t qn = in ? nd.nxt[x] : INF32;
+            warp_bits(nres_a, qn != INF32, qn, false);
           }
-          res_pos[lid] = NONE;
-          hs += splitmix64(eh | lid);
+          if (in) {
+            res_pos[lid] = NONE;
+            hs += splitmix64(eh | lid);
+          }
         }
         const unsigned long long nvp = block_reduce<RT, unsigned long long>(
             ((unsigned long long)n_direct << 32) | n_prot, Add(), sm.b, par);
@@ -785,9 +862,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         for (int u = 0; u < UNR; ++u) {
           const uint64_t pb = wb + (uint64_t)u * RT + lane;
           const bool in = pb >= P0 && pb < P1;
-          q[u] = in ? nd.nxt[pb] : 0u;
-          lf[u] = in ? nd.lidf[pb] : 0u;
-          uo[u] = (in && !belady) ? nd.u_of[pb] : 0u;
+          q[u] = in ? P(2, pb) : 0u;
+          lf[u] = in ? P(0, pb) : 0u;
+          uo[u] = (in && !belady) ? P(1, pb) : 0u;
           last[u] = in && (uint64_t)q[u] >= P1;  // INF included
         }
 #pragma unroll
@@ -796,7 +873,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           const uint32_t lid = lf[u] & LID_MASK;
           if (last[u]) res_pos[lid] = (uint32_t)pb;
           if (belady) {
-            if (last[u] && q[u] == INF32) hb_set(dead, lid);
+            hb_update_warp(dead, last[u] && q[u] == INF32, lid, true);
             hb_update_warp(pend, last[u] && q[u] != INF32, q[u], true);
             const uint32_t md = __ballot_sync(0xffffffffu, last[u] && q[u] == INF32);
             const uint32_t mp = __ballot_sync(0xffffffffu, last[u] && q[u] != INF32);
@@ -805,11 +882,8 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             const uint32_t wv = __ballot_sync(0xffffffffu, last[u]);
             if (lane == 0 && wv) atomicOr(&alive[(wb + (uint64_t)u * RT) >> 5], wv);
             const uint32_t un = uo[u] & UMASK;
-            if (last[u]) {
-              if (q[u] != INF32) atomicOr(&nres_a[q[u] >> 5], 1u << (q[u] & 31));
-              const uint32_t pr = __match_any_sync(wv, un);
-              if (lane == 31 - __clz(pr)) atomicAdd(&cnt[un], (uint32_t)__popc(pr));
-            }
+            warp_bits(nres_a, last[u] && q[u] != INF32, q[u], true);
+            warp_count(cnt, last[u], un, true);
           }
         }
       }
@@ -850,6 +924,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       c_events += 1;
     }
     // ---- counters ----
+    if (pf_j != NONE) await_pf();  // no bulk copy may target the staging area after the item
     __syncthreads();
     {
       unsigned long long* sc = reinterpret_cast<unsigned long long*>(s_ctr);
@@ -1160,6 +1235,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   uint64_t dyn = std::max<uint64_t>(std::max<uint64_t>(dyn_b, dyn_a), a.ocall_smem ? oc_bytes : 16);
   dyn = (dyn + 15) & ~15ull;
   a.dyn_words = (uint32_t)(dyn / 4);
+  dyn += (uint64_t)PF_WORDS * 4;  // TMA staging area in front
   SAGA_CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);

@@ -155,7 +155,8 @@ template <class T>
 T* dalloc(saga_trace* t, size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
-  if (ws_malloc(&p, n * sizeof(T), t->stream) != cudaSuccess) return nullptr;
+  // 64 bytes of slack: 16-byte TMA bulk copies may round a range's end up past element n - 1
+  if (ws_malloc(&p, n * sizeof(T) + 64, t->stream) != cudaSuccess) return nullptr;
   t->allocs.push_back(p);
   return static_cast<T*>(p);
 }
