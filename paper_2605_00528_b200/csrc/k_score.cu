@@ -18,6 +18,8 @@ namespace saga {
 namespace {
 
 constexpr int ST = 1024;
+constexpr int SW = ST / 32;  // warps per CTA
+constexpr int SU = 4;        // 32-candidate chunks whose loads are issued together
 
 struct ScoreNode { const uint32_t* lown; uint32_t n_local; };
 
@@ -65,6 +67,7 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
   __shared__ BlockScratch<ST> sm;
   Par par;
   const TraceView& v = a.v;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t sg = blockIdx.x; sg < a.b.n_seg; sg += gridDim.x) {
     const uint64_t c0 = a.b.seg_off[sg], c1 = a.b.seg_off[sg + 1];
     const uint32_t w = a.b.seg_node[sg];
@@ -72,24 +75,42 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
     const int64_t Te = (int64_t)e * v.epoch_us;
     if (a.b.policy == SAGA_POLICY_BELADY) {
       for (uint64_t i = c0 + threadIdx.x; i < c1; i += ST)
-        a.key[i] = ((uint64_t)__ldcs(&a.b.cand_nu[i]) << 32) | __ldcs(&a.b.cand_lid[i]);
+        __stcs(&a.key[i], ((uint64_t)__ldcs(&a.b.cand_nu[i]) << 32) | __ldcs(&a.b.cand_lid[i]));
       continue;
     }
     const uint32_t* lown = a.nodes[w].lown;
     const uint32_t act = a.b.seg_act[sg];
     const uint32_t C = a.b.seg_cap[sg], occ = a.b.seg_occ[sg];
-    // pass 1: normalisers
+    // Each warp owns a contiguous slab of the segment and walks it 32 consecutive candidates at
+    // a time (coalesced), so the owner (a run of one session's blocks) rarely changes within a
+    // lane's sequence and its state is looked up once per run.
+    const uint64_t n = c1 - c0;
+    const uint64_t slab = ((n + SW - 1) / SW + 31) & ~31ull;
+    const uint64_t w0 = c0 + (uint64_t)wid * slab, w1 = min(c1, w0 + slab);
+    // pass 1: normalisers (eq:recency tau_max, eq:size size_max)
     long long tau = 0;
     uint32_t smax = 1;
     uint32_t last_o = NONE, last_sz = 0;
-    for (uint64_t i = c0 + threadIdx.x; i < c1; i += ST) {
-      tau = max(tau, (long long)(Te - a.b.cand_t_last[i]));
-      const uint32_t o = __ldg(&lown[a.b.cand_lid[i]]);
-      if (o != last_o) {
-        last_o = o;
-        last_sz = o >= v.n_sessions ? __ldg(&v.tlen[o - v.n_sessions]) : __ldg(&v.ci_size[cstar(v, o, e)]);
+    for (uint64_t b = w0; b < w1; b += 32 * SU) {
+      uint32_t lid[SU];
+      int64_t tl[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const uint64_t i = b + (uint64_t)u * 32 + lane;
+        lid[u] = i < w1 ? __ldcs(&a.b.cand_lid[i]) : NONE;
+        tl[u] = i < w1 ? a.b.cand_t_last[i] : Te;
       }
-      smax = max(smax, last_sz);
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        if (lid[u] == NONE) continue;
+        tau = max(tau, (long long)(Te - tl[u]));
+        const uint32_t o = __ldg(&lown[lid[u]]);
+        if (o != last_o) {
+          last_o = o;
+          last_sz = o >= v.n_sessions ? __ldg(&v.tlen[o - v.n_sessions]) : __ldg(&v.ci_size[cstar(v, o, e)]);
+        }
+        smax = max(smax, last_sz);
+      }
     }
     tau = block_reduce<ST, long long>(tau, Max(), sm, par);
     smax = block_reduce<ST, uint32_t>(smax, Max(), sm, par);
@@ -98,24 +119,35 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
     x.den = (int64_t)(a.p_high - a.p_low) * C;
     x.num = min(x.den, max((int64_t)0, 1000 * (int64_t)occ - (int64_t)a.p_low * C));
     x.ttl_max = a.ttl_max; x.alpha = a.alpha; x.beta = a.beta; x.gamma = a.gamma;
-    // pass 2: keys
+    // pass 2: keys (the slab re-read hits L2)
     last_o = NONE;
     OwnerKeyIn oi{};
-    for (uint64_t i = c0 + threadIdx.x; i < c1; i += ST) {
-      const uint32_t lid = __ldcs(&a.b.cand_lid[i]);
-      const int64_t tl = __ldcs(&a.b.cand_t_last[i]);
-      const uint32_t o = __ldg(&lown[lid]);
-      if (o != last_o) { last_o = o; oi = owner_at(v, o, e, act); }
-      const float sc = wa_lru_score(x, tl, oi.size, oi.P);
-      __stcs(&a.key[i], aeg_key(ttl_protected(x, oi), quantize_q20(sc), lid));
-      if (a.score) __stcs(&a.score[i], sc);
+    for (uint64_t b = w0; b < w1; b += 32 * SU) {
+      uint32_t lid[SU];
+      int64_t tl[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const uint64_t i = b + (uint64_t)u * 32 + lane;
+        lid[u] = i < w1 ? __ldcs(&a.b.cand_lid[i]) : NONE;
+        tl[u] = i < w1 ? __ldcs(&a.b.cand_t_last[i]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        if (lid[u] == NONE) continue;
+        const uint64_t i = b + (uint64_t)u * 32 + lane;
+        const uint32_t o = __ldg(&lown[lid[u]]);
+        if (o != last_o) { last_o = o; oi = owner_at(v, o, e, act); }
+        const float sc = wa_lru_score(x, tl[u], oi.size, oi.P);
+        __stcs(&a.key[i], aeg_key(ttl_protected(x, oi), quantize_q20(sc), lid[u]));
+        if (a.score) __stcs(&a.score[i], sc);
+      }
     }
     __syncthreads();
   }
 }
 
 // ---------------- bulk select ----------------
-constexpr int SLT = 1024;
+constexpr int SLT = 512;  // several segments per SM: a segment's passes are latency-bound
 
 __device__ void bitonic_desc(uint64_t* k, uint32_t* idx, uint32_t n_pow2) {
   for (uint32_t size = 2; size <= n_pow2; size <<= 1) {
@@ -140,12 +172,27 @@ __device__ void bitonic_desc(uint64_t* k, uint32_t* idx, uint32_t n_pow2) {
   }
 }
 
+constexpr uint32_t KMAX = 2048;  // winners and pivot bucket held in shared memory
+constexpr int SEL_U = 8;         // keys per thread whose loads are issued together
+
+// One CTA per segment.  pass 1: OR / AND of the keys (the one HBM read); pass 2: histogram of the
+// 11 bits below the highest differing bit; pass 3: keys in digits above the pivot digit are
+// winners, keys in the pivot digit are gathered; both lists live in shared memory, the pivot list
+// is sorted to take the remaining winners and the winners are sorted.  Passes 2-3 re-read L2.
+// Segments whose winners or pivot bucket exceed KMAX take the general path (radix select + a
+// bitonic sort in global scratch).
 __global__ void __launch_bounds__(SLT) k_select(const uint64_t* __restrict__ key, const uint64_t* __restrict__ seg_off,
                                                 const uint32_t* __restrict__ kreq, uint32_t n_seg,
                                                 const uint64_t* __restrict__ out_off, uint32_t* __restrict__ victim,
                                                 uint64_t* scratch_k, uint32_t* scratch_i, uint64_t scratch_per_cta) {
   __shared__ BlockScratch<SLT> sm;
-  __shared__ uint32_t s_cnt;
+  __shared__ uint32_t hist[2048];
+  extern __shared__ __align__(16) uint64_t sel_dyn[];  // winners / pivot lists (96 KB)
+  uint64_t* wk = sel_dyn;
+  uint64_t* pk = wk + KMAX;
+  uint32_t* wix = reinterpret_cast<uint32_t*>(pk + KMAX);
+  uint32_t* pix = wix + KMAX;
+  __shared__ uint32_t s_cnt, s_np, s_d, s_above;
   Par par;
   uint64_t* sk = scratch_k + (uint64_t)blockIdx.x * scratch_per_cta;
   uint32_t* si = scratch_i + (uint64_t)blockIdx.x * scratch_per_cta;
@@ -156,6 +203,98 @@ __global__ void __launch_bounds__(SLT) k_select(const uint64_t* __restrict__ key
     if (k > n) k = n;
     if (k == 0) continue;
     const uint64_t* kb = key + c0;
+    const uint64_t o = out_off[sg];
+    bool fast = false;
+    if (k < n && k <= KMAX) {
+      // pass 1
+      unsigned long long orv = 0, anv = ~0ull;
+      for (uint32_t b = threadIdx.x; b < n; b += SLT * SEL_U) {
+        uint64_t x[SEL_U];
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u) x[u] = b + u * SLT < n ? __ldcg(&kb[b + u * SLT]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u) if (b + u * SLT < n) { orv |= x[u]; anv &= x[u]; }
+      }
+      orv = block_reduce<SLT, unsigned long long>(orv, Or(), sm, par);
+      anv = block_reduce<SLT, unsigned long long>(anv, And(), sm, par);
+      const unsigned long long diff = orv ^ anv;  // != 0: keys are unique and n > k >= 1
+      const int top = 63 - __clzll(diff);
+      const int width = min(11, top + 1);
+      const int shift = top + 1 - width;
+      const uint32_t dm = (1u << width) - 1u;
+      // pass 2
+      for (uint32_t i = threadIdx.x; i < 2048; i += SLT) hist[i] = 0;
+      __syncthreads();
+      for (uint32_t b = threadIdx.x; b < n; b += SLT * SEL_U) {
+        uint64_t x[SEL_U];
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u) x[u] = b + u * SLT < n ? __ldcg(&kb[b + u * SLT]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u)
+          if (b + u * SLT < n) atomicAdd(&hist[(uint32_t)(x[u] >> shift) & dm], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {  // pivot digit: the k-th largest key lies in it
+        const int lane = threadIdx.x;
+        uint32_t sum = 0;
+        for (int q = 0; q < 64; ++q) sum += hist[2047 - (lane * 64 + q)];
+        uint32_t x = sum;
+#pragma unroll
+        for (int of = 1; of < 32; of <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, of);
+          if (lane >= of) x += y;
+        }
+        uint32_t c = x - sum;
+        if (c < k && k <= x) {
+          for (int q = 0; q < 64; ++q) {
+            const uint32_t h = hist[2047 - (lane * 64 + q)];
+            if (c < k && k <= c + h) { s_d = 2047u - (lane * 64u + q); s_above = c; }
+            c += h;
+          }
+        }
+      }
+      __syncthreads();
+      const uint32_t d = s_d, A = s_above, B = hist[d];
+      fast = A <= KMAX && B <= KMAX;
+      if (fast) {
+        if (threadIdx.x == 0) { s_cnt = 0; s_np = 0; }
+        __syncthreads();
+        // pass 3
+        for (uint32_t b = threadIdx.x; b < n; b += SLT * SEL_U) {
+          uint64_t x[SEL_U];
+#pragma unroll
+          for (int u = 0; u < SEL_U; ++u) x[u] = b + u * SLT < n ? __ldcg(&kb[b + u * SLT]) : 0ull;
+#pragma unroll
+          for (int u = 0; u < SEL_U; ++u) {
+            const uint32_t i = b + u * SLT;
+            if (i >= n) continue;
+            const uint32_t dg = (uint32_t)(x[u] >> shift) & dm;
+            if (dg > d) { const uint32_t p = atomicAdd(&s_cnt, 1u); wk[p] = x[u]; wix[p] = i; }
+            else if (dg == d) { const uint32_t p = atomicAdd(&s_np, 1u); pk[p] = x[u]; pix[p] = i; }
+          }
+        }
+        __syncthreads();
+        // Rank the candidates: every winner (digit above the pivot digit) outranks every pivot-digit
+        // key, so a winner's rank is its rank among the winners and a pivot key's is A plus its
+        // rank in the pivot digit.  Keys are unique: rank < k selects the k largest, in order.
+        for (uint32_t i = threadIdx.x; i < A + B; i += SLT) {
+          uint32_t r = 0;
+          if (i < A) {
+            const uint64_t x = wk[i];
+            for (uint32_t j = 0; j < A; ++j) r += wk[j] > x;
+            victim[o + r] = wix[i];
+          } else {
+            const uint64_t x = pk[i - A];
+            r = A;
+            for (uint32_t j = 0; j < B; ++j) r += pk[j] > x;
+            if (r < k) victim[o + r] = pix[i - A];
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (fast) continue;
+    // general path
     const uint64_t T = (k < n) ? radix_select<SLT>(kb, n, k, sm, par) : 0ull;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
@@ -173,7 +312,6 @@ __global__ void __launch_bounds__(SLT) k_select(const uint64_t* __restrict__ key
     for (uint32_t i = k + threadIdx.x; i < np2; i += SLT) { sk[i] = 0; si[i] = 0xFFFFFFFFu; }  // padding sorts last
     __syncthreads();
     bitonic_desc(sk, si, np2);
-    const uint64_t o = out_off[sg];
     for (uint32_t i = threadIdx.x; i < k; i += SLT) victim[o + i] = si[i];
     __syncthreads();
   }
@@ -222,13 +360,17 @@ saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint3
   for (uint32_t i = 0; i < n_seg; ++i) mx = std::max<uint64_t>(mx, off[i + 1] - off[i]);
   uint64_t np2 = 1;
   while (np2 < mx) np2 <<= 1;
-  const unsigned grid = std::min<unsigned>(n_seg, nsm_count());
+  const size_t dyn = (size_t)KMAX * (8 + 8 + 4 + 4);
+  SAGA_CK(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_select, SLT, dyn);
+  const unsigned grid = std::min<unsigned>(n_seg, nsm_count() * (unsigned)std::max(occ, 1));
   uint64_t* sk = nullptr;
   uint32_t* si = nullptr;
   SAGA_CK(ws_malloc((void**)&sk, 8 * np2 * grid, s));
   SAGA_CK(ws_malloc((void**)&si, 4 * np2 * grid, s));
   prof_begin(SAGA_PROF_SELECT, s);
-  k_select<<<grid, SLT, 0, s>>>(key, seg_off, k, n_seg, out_off, victim, sk, si, np2);
+  k_select<<<grid, SLT, dyn, s>>>(key, seg_off, k, n_seg, out_off, victim, sk, si, np2);
   prof_end(SAGA_PROF_SELECT, s);
   count_launch();
   SAGA_CK_LAUNCH();

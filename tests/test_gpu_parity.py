@@ -219,6 +219,39 @@ def test_select_equal():
         assert np.array_equal(g[out_off[i]:out_off[i + 1]], ref), i
 
 
+@pytest.mark.parametrize("clustered", [False, True])
+def test_select_equal_shared_memory_path(clustered):
+    """k <= 4096 with a pivot digit of <= 4096 keys runs the shared-memory path; k > 4096 or a
+    crowded pivot digit runs the general path.  Both must equal the full descending sort."""
+    rng = np.random.default_rng(11 + clustered)
+    cases = [(32768, 1), (32768, 5), (32768, 327), (32768, 4096), (32768, 4097), (9000, 8999), (9000, 9000),
+             (4096, 2048), (70000, 700), (3, 2)]
+    keys, ks, offs = [], [], [0]
+    for n, k in cases:
+        if clustered:  # equal high bits: one protection bit and q, lids differ
+            x = np.uint64(0x8000002A00000000) | rng.choice(2 ** 22, size=n, replace=False).astype(np.uint64)
+        else:
+            x = np.unique(rng.integers(0, 2 ** 64 - 1, size=n * 2, dtype=np.uint64))[:n]
+        rng.shuffle(x)
+        keys.append(x)
+        ks.append(k)
+        offs.append(offs[-1] + n)
+    allk = np.concatenate(keys)
+    out_off = np.concatenate([[0], np.cumsum(ks)]).astype(np.int64)
+    dev = "cuda"
+    vk = torch.from_numpy(allk.view(np.int64).copy()).to(dev)
+    so = torch.from_numpy(np.array(offs, np.int64)).to(dev)
+    kk = torch.from_numpy(np.array(ks, np.int32)).to(dev)
+    oo = torch.from_numpy(out_off).to(dev)
+    vic = torch.full((int(out_off[-1]),), -1, dtype=torch.int32, device=dev)
+    saga.evict_select(vk, so, kk, oo, vic)
+    torch.cuda.synchronize()
+    g = vic.cpu().numpy()
+    for i, x in enumerate(keys):
+        ref = O.select_topk(x, ks[i])
+        assert np.array_equal(g[out_off[i]:out_off[i + 1]], ref), (i, cases[i])
+
+
 def test_invalid_trace_rejected():
     d = make_c1()
     d.call_t_us = d.call_t_us.copy()
