@@ -119,8 +119,8 @@ typedef struct {
 /* Placement configuration (DESIGN.md R-load, R-steal): 100 ms epochs, kappa
  * concurrent requests per node, theta and R_max in per-mille, T_idle. */
 typedef struct {
-  int64_t epoch_us;        /* 100000 */
-  uint32_t kappa;          /* 32     */
+  int64_t epoch_us;        /* 100000; must be in (0, 1e9] (SAGA_ERR_INVALID_ARG otherwise) */
+  uint32_t kappa;          /* 32; at most 256 */
   uint32_t prefill_tok_s;  /* 5000 */
   uint32_t decode_tok_s;   /* 30 */
   uint32_t theta_pm;       /* 800  */
@@ -215,7 +215,8 @@ saga_status saga_aeg_score(const saga_trace* t, const saga_score_batch* batch, c
 /* A6.  For each segment i of keys [seg_off_dev[i], seg_off_dev[i+1]) select the k_dev[i] largest
  * keys (keys must be unique within a segment) and write their indices relative to the segment
  * start, in descending key order, to victim_idx_dev[out_off_dev[i] ...].  k > segment size
- * is clamped (the tail of the output range is left untouched). */
+ * is clamped (the tail of the output range is left untouched).  Syncs once before the launch
+ * (reads seg_off_dev to size the scratch of segments whose winners exceed shared memory). */
 saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_dev, const uint32_t* k_dev,
                               uint32_t n_seg, const uint64_t* out_off_dev, uint32_t* victim_idx_dev,
                               saga_stream_t stream);
@@ -226,7 +227,10 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
  * the order AEG, BELADY, EVICT_ALL; cells of nodes not listed are left untouched (zero them
  * first; then an all-reduce sum over ranks is an exact gather).  A capacity below a node's
  * W_lo is data, not an error: INFEASIBLE_EPOCH is set and that replay stops counting.
- * SAGA_ERR_CAPACITY if a capacity is 0. */
+ * SAGA_ERR_CAPACITY if a capacity is 0.  Syncs: the first call for a node builds its replay
+ * index (units, event ranges) and every call checks the kernel's internal invariants
+ * (SAGA_ERR_STATE with the failing check in saga_last_error()).  Set SAGA_REPLAY_TRACE=1 to
+ * print per-item / per-phase SM cycles to stderr. */
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream);
 

@@ -122,15 +122,21 @@ __global__ void k_ev_pos(const uint64_t* g_pos, const uint32_t* ev_g, uint32_t J
 __global__ void __launch_bounds__(SS_T) k_epoch_stats(const uint32_t* __restrict__ nxt, uint32_t* lidf, uint64_t n,
                                                       const uint64_t* __restrict__ ev_pos, uint32_t J,
                                                       uint32_t* cnt_dist, uint32_t* cnt_first, uint32_t* cnt_last) {
+  __shared__ uint32_t s_j0;
+  const uint64_t t0 = (uint64_t)blockIdx.x * SS_T * SS_ITEMS;
+  if (threadIdx.x == 0) {  // event containing the tile's first position: last j with ev_pos[j] <= t0
+    uint32_t lo = 0, hi = J;
+    while (lo + 1 < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (ev_pos[mid] <= t0) lo = mid; else hi = mid;
+    }
+    s_j0 = lo;
+  }
+  __syncthreads();
   const uint64_t p0 = ((uint64_t)blockIdx.x * SS_T + threadIdx.x) * SS_ITEMS;
   if (p0 >= n) return;
-  // event containing p0: last j with ev_pos[j] <= p0
-  uint32_t lo = 0, hi = J;
-  while (lo + 1 < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (ev_pos[mid] <= p0) lo = mid; else hi = mid;
-  }
-  uint32_t j = lo;
+  uint32_t j = s_j0;  // a tile spans few events: walk forward to the one containing p0
+  while (ev_pos[j + 1] <= p0) ++j;
   uint64_t end = ev_pos[j + 1];
   uint32_t cd = 0, cf = 0, cl = 0;
   for (int i = 0; i < SS_ITEMS; ++i) {
@@ -156,15 +162,16 @@ __global__ void __launch_bounds__(SS_T) k_epoch_stats(const uint32_t* __restrict
 }
 
 // W_lo = max distinct; W_hi = max_j (sum_{i<=j} first_i - sum_{i<j} last_i)   (one CTA)
+constexpr int SW_T = 1024;
 __global__ void k_sweep(const uint32_t* cnt_dist, const uint32_t* cnt_first, const uint32_t* cnt_last, uint32_t Jr,
                         uint32_t* out /*[2]*/) {
   __shared__ long long s_carry_f, s_carry_l;
   __shared__ uint32_t s_lo, s_hi;
-  __shared__ long long wf[SS_T / 32], wl[SS_T / 32];
+  __shared__ long long wf[SW_T / 32], wl[SW_T / 32];
   if (threadIdx.x == 0) { s_carry_f = 0; s_carry_l = 0; s_lo = 0; s_hi = 0; }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (uint32_t b = 0; b < Jr; b += SS_T) {
+  for (uint32_t b = 0; b < Jr; b += SW_T) {
     const uint32_t j = b + threadIdx.x;
     long long f = j < Jr ? cnt_first[j] : 0, l = j < Jr ? cnt_last[j] : 0;
     uint32_t dist = j < Jr ? cnt_dist[j] : 0;
@@ -185,16 +192,17 @@ __global__ void k_sweep(const uint32_t* cnt_dist, const uint32_t* cnt_first, con
       atomicMax(&s_hi, (uint32_t)(F - Lex));
     }
     __syncthreads();
-    if (threadIdx.x == SS_T - 1) { s_carry_f = pf + xf; s_carry_l = pl + xl; }
+    if (threadIdx.x == SW_T - 1) { s_carry_f = pf + xf; s_carry_l = pl + xl; }
     __syncthreads();
   }
   if (threadIdx.x == 0) { out[0] = s_lo; out[1] = s_hi; }
 }
 
+// owners come in runs of consecutive local ids: only the first id of a run sets the bit
 __global__ void k_present(const uint32_t* lown, uint32_t n_local, uint32_t n_sessions, uint32_t* present) {
   for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_local; l += gridDim.x * blockDim.x) {
-    uint32_t o = lown[l];
-    if (o < n_sessions) atomicOr(&present[o >> 5], 1u << (o & 31));
+    const uint32_t o = lown[l];
+    if (o < n_sessions && (l == 0 || lown[l - 1] != o)) atomicOr(&present[o >> 5], 1u << (o & 31));
   }
 }
 __global__ void k_flag_present(const uint32_t* call_sess, uint32_t n_calls, const uint32_t* present, uint32_t* flag) {
@@ -274,7 +282,7 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
       k_epoch_stats<<<(unsigned)((N + SS_TILE - 1) / SS_TILE), SS_T, 0, s>>>(nd.nxt, nd.lidf, N, ev_pos, J, cd, cf, cl);
       count_launch();
     }
-    k_sweep<<<1, SS_T, 0, s>>>(cd, cf, cl, Jr, sw);
+    k_sweep<<<1, SW_T, 0, s>>>(cd, cf, cl, Jr, sw);
     prof_end(SAGA_PROF_EPOCH, s);
     count_launch();
     uint32_t hw[2] = {0, 0}, hn = 0;
