@@ -58,12 +58,13 @@ struct __align__(8) UnitRec {
   int64_t t;        // t_last of its blocks: t_c of the CALL group, T_e of a MIG group
   uint32_t pa, pe;  // positions [pa, pe)
   uint32_t lo;      // local owner id (private session) or LO_SHARED | type
-  uint32_t pad;
+  uint32_t flags;   // U_MONO: local ids strictly increase with position inside the unit
 };
+constexpr uint32_t U_MONO = 1u;
 // live-list entry: the unit record plus the per-event key part
 struct __align__(16) ListRec {
   int64_t t;
-  uint32_t u, pa, pe, lo, kp, pad;
+  uint32_t u, pa, pe, lo, kp, flags;
 };
 // per-call inputs of the WA-LRU key of a private session whose newest call is c
 struct __align__(8) CallKey {
@@ -131,7 +132,7 @@ struct Smem {
   uint32_t hist[H1];
   uint32_t res_j, res_rem, thr, item;
   uint32_t hb_j2, hb_j1;
-  uint32_t n_app, n_piv, n_vict, n_vu;
+  uint32_t n_app, n_piv, n_vict, n_vu, n_pu, pu_i;
   uint32_t ilo, ihi;
   uint32_t tot_dead, tot_pend;  // BELADY: set bits of the two hierarchical bitmaps
   __align__(8) uint64_t pbar[2];  // TMA prefetch stages of per-position arrays
@@ -751,7 +752,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             const uint32_t kps = ((d1 >> 11) << 31) | ((d1 & 2047u) << 10) | d2;
             const bool prot_piv = !(kps >> 31);
             const bool whole = sm.hist[d2] == r2;  // the pivot units are evicted whole
-            if (threadIdx.x == 0) { sm.n_piv = 0; sm.n_vu = 0; }
+            if (threadIdx.x == 0) { sm.n_piv = 0; sm.n_vu = 0; sm.n_pu = 0; }
             __syncthreads();
             PH(3);
             // pass c: list the entries with kp >= kp* (flat), then evict units above the pivot
@@ -759,6 +760,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             for (uint32_t i = threadIdx.x; i < ((nL + 31) & ~31u); i += RT) {
               bool vic = false;
               if (i < nL) vic = L[i].kp >= kps && cnt[L[i].u] != 0;
+              if (vic && L[i].kp == kps) { atomicAdd(&sm.n_pu, 1u); sm.pu_i = i; }
               const uint32_t vm = __ballot_sync(0xffffffffu, vic);
               uint32_t b0 = 0;
               if (lane == 0 && vm) b0 = atomicAdd(&sm.n_vu, (uint32_t)__popc(vm));
@@ -767,9 +769,42 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             }
             __syncthreads();
             const uint32_t nvu = sm.n_vu;
+            // one pivot unit whose local ids increase with position: its r2 largest lids are its
+            // r2 highest resident positions -- no ranking needed
+            const bool mono_piv = !whole && sm.n_pu == 1 && (L[sm.pu_i].flags & U_MONO);
             for (uint32_t q = wid; q < nvu; q += RW) {
               const ListRec r = L[vunits[q]];
               if (r.kp > kps || whole) { evict_unit(r.u, r.pa, r.pe, !(r.kp >> 31)); continue; }
+              if (mono_piv) {
+                const uint32_t wfirst = r.pa >> 5, wlast = (r.pe - 1) >> 5;
+                uint32_t need = r2;  // take from the top word down
+                for (int64_t wb = (int64_t)wlast - 31; need > 0; wb -= 32) {
+                  const int64_t wi = wb + lane;
+                  const uint32_t wv = (wi >= (int64_t)wfirst && wi <= (int64_t)wlast)
+                                          ? (alive[wi] & unit_mask((uint32_t)wi, r.pa, r.pe)) : 0u;
+                  const uint32_t c = __popc(wv);
+                  uint32_t xs = c;  // inclusive suffix sum from lane 31 down
+#pragma unroll
+                  for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_down_sync(0xffffffffu, xs, o);
+                    if (lane + o < 32) xs += y;
+                  }
+                  const uint32_t above = xs - c;  // resident positions in higher words of the chunk
+                  uint32_t tk = 0;
+                  if (above < need) {
+                    tk = wv;
+                    const uint32_t keep = above + c > need ? above + c - need : 0u;  // lowest bits stay
+                    for (uint32_t z = 0; z < keep; ++z) tk &= tk - 1;
+                  }
+                  if (tk) atomicAnd(&alive[wi], ~tk);
+                  emit_bits(vlist, &sm.n_vict, (uint32_t)(wi > 0 ? wi : 0), tk, 0u);
+                  const uint32_t tot = __shfl_sync(0xffffffffu, xs, 0);
+                  need = tot >= need ? 0u : need - tot;
+                  if (wb <= (int64_t)wfirst) break;
+                }
+                if (lane == 0) { cnt[r.u] -= r2; if (prot_piv) n_prot += r2; }
+                continue;
+              }
               const uint32_t wlast = (r.pe - 1) >> 5;
               for (uint32_t wb = (r.pa >> 5); wb <= wlast; wb += 32) {
                 const uint32_t wi = wb + lane;
@@ -791,7 +826,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             __syncthreads();
             const uint32_t npv = sm.n_piv;
             if (threadIdx.x == 0 && npv > C) dbg_fail(a.dbg, __LINE__, npv, C, r2);
-            if (!whole && npv) {
+            if (!whole && !mono_piv && npv) {
               // pivot keys differ only in lid: rank (lid << 32 | slot) and keep the top r2
               uint32_t* pslot = vlist + k;  // (unit, position) of gathered slot i, after the list
               for (uint32_t i = threadIdx.x; i < npv; i += RT) {
@@ -905,7 +940,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             } else {
               const uint32_t u = U0 + (i - nL);
               const UnitRec ur = nd.urec[u];
-              r.t = ur.t; r.u = u; r.pa = ur.pa; r.pe = ur.pe; r.lo = ur.lo; r.kp = 0; r.pad = 0;
+              r.t = ur.t; r.u = u; r.pa = ur.pa; r.pe = ur.pe; r.lo = ur.lo; r.kp = 0; r.flags = ur.flags;
             }
             keep = cnt[r.u] != 0;
           }
@@ -1017,9 +1052,16 @@ __global__ void k_unit_fill(const uint32_t* head, const uint32_t* hpos, uint64_t
     r.pa = (uint32_t)p;
     r.pe = 0;
     r.lo = own < n_sessions ? s2lo[own] : (LO_SHARED | (own - n_sessions));
-    r.pad = 0;
+    r.flags = U_MONO;
     urec[u] = r;
     u_kind[u] = g_kind[lo];
+  }
+}
+// a unit loses U_MONO where a local id does not increase from one position to the next
+__global__ void k_unit_mono(const uint32_t* lidf, const uint32_t* u_of, uint64_t N, UnitRec* urec) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p + 1 < N; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = u_of[p] & UMASK;
+    if ((u_of[p + 1] & UMASK) == u && (lidf[p + 1] & LID_MASK) <= (lidf[p] & LID_MASK)) atomicAnd(&urec[u].flags, ~U_MONO);
   }
 }
 __global__ void k_unit_end(const uint32_t* u_pos, uint32_t n_units, uint64_t N, UnitRec* urec) {
@@ -1127,7 +1169,8 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
     k_unit_end<<<grid_for(nu), NTHREADS, 0, s>>>(u_pos, nu, N, ur);
     k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(hpos, N, u_kind, nd.u_of);
     k_prev_unit<<<grid_for(N), NTHREADS, 0, s>>>(nd.prv, nd.u_of, N, nd.upu);
-    count_launch(4);
+    k_unit_mono<<<grid_for(N), NTHREADS, 0, s>>>(nd.lidf, nd.u_of, N, ur);
+    count_launch(5);
   }
   k_ev_index<<<grid_for(std::max<size_t>(size_t(J) + 1, nd.n_upd)), NTHREADS, 0, s>>>(
       v, nd.ev_pos, nd.ev_e, J, hpos, N, nu, nd.upd_c, nd.n_upd, s2lo, nd.ev_unit, nd.ev_upd, nd.upd_lo);
