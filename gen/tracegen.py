@@ -712,15 +712,16 @@ def make_random_small(seed: int, n_sessions: int = 5, n_nodes: int = 2, max_call
         type_shared_len=np.array(shared, np.uint32), **aeg)
 
 
-def make_stream_trace(seq, epochs=None, n_nodes: int = 1) -> TraceDesc:
+def make_stream_trace(seq, epochs=None, n_nodes: int = 1, n_shared: int = 0) -> TraceDesc:
     """A one-node trace whose node-0 stream is exactly `seq` (block ids): access i is a one-block
     call of a single session at boundary epochs[i] (default: every access in its own epoch).
+    Blocks 0 .. n_shared-1 are the shared prefix of the session's agent type, the rest its own.
     Used to feed hand-written access sequences (e.g. SPEC S:252 "A B C A B") to next-use / MIN."""
     seq = [int(x) for x in seq]
     n = len(seq)
     if epochs is None:
         epochs = list(range(1, n + 1))
-    nb = max(seq) + 1 if seq else 1
+    nb = max(max(seq) + 1 if seq else 1, n_shared)
     b = _AEGBuilder()
     b.add_node(1_000_000, 0, False)
     aeg = b.finish()
@@ -732,5 +733,6 @@ def make_stream_trace(seq, epochs=None, n_nodes: int = 1) -> TraceDesc:
         call_new_tokens=np.full(n, 16, np.uint32), call_is_last=np.zeros(n, np.uint8),
         call_range_off=np.arange(n + 1, dtype=np.uint32), range_block_lo=np.array(seq, np.uint32),
         range_len=np.ones(n, np.uint32), session_type=np.zeros(1, np.uint16),
-        session_block_lo=np.zeros(1, np.uint32), session_block_len=np.array([nb], np.uint32),
-        type_shared_lo=np.array([0], np.uint32), type_shared_len=np.array([0], np.uint32), **aeg)
+        session_block_lo=np.array([n_shared], np.uint32),
+        session_block_len=np.array([max(nb - n_shared, 0)], np.uint32),
+        type_shared_lo=np.array([0], np.uint32), type_shared_len=np.array([n_shared], np.uint32), **aeg)

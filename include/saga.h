@@ -53,7 +53,11 @@ typedef enum {
 typedef enum {
   SAGA_POLICY_AEG = 1,      /* WA-LRU with AEG predictions (eq:eviction) + tool-call TTL (Alg. 1) */
   SAGA_POLICY_BELADY = 2,   /* epoch-batched farthest-next-use (Belady)                  */
-  SAGA_POLICY_EVICT_ALL = 4 /* test policy: evict every non-requested block each epoch (Obs. 1)  */
+  SAGA_POLICY_EVICT_ALL = 4, /* test policy: evict every non-requested block each epoch (Obs. 1) */
+  SAGA_POLICY_LRU = 8,       /* baseline "Standard LRU" of Table tab:competitive: the
+                                block whose latest access is earliest in the node stream goes first */
+  SAGA_POLICY_LRU_PREFIX = 16 /* baseline "LRU + Prefix (vLLM v0.5)": LRU over private blocks;
+                                shared-prefix blocks only when no private candidate is left */
 } saga_policy;
 
 /* Counter slots, int64 each, 16 per (policy, capacity, node) replay (DESIGN.md §5 "Counters").
@@ -224,7 +228,7 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
 /* A7.  Replays policies x caps x nodes.  caps (host, n_caps) uniform across nodes; nodes (host,
  * n_owned) must be owned and have had saga_belady_next_use.  counters_dev is
  * int64[n_pol][n_caps][n_nodes][SAGA_NCOUNT] with n_pol = popcount(policy_mask), policies in
- * the order AEG, BELADY, EVICT_ALL; cells of nodes not listed are left untouched (zero them
+ * the order AEG, BELADY, EVICT_ALL, LRU, LRU_PREFIX; cells of nodes not listed are left untouched (zero them
  * first; then an all-reduce sum over ranks is an exact gather).  A capacity below a node's
  * W_lo is data, not an error: INFEASIBLE_EPOCH is set and that replay stops counting.
  * SAGA_ERR_CAPACITY if a capacity is 0.  Syncs: the first call for a node builds its replay

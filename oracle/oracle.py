@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "saga_oracle.cpp")
 LIB = os.path.join(HERE, "libsaga_oracle.so")
 
-POL_AEG, POL_BELADY, POL_EVICT_ALL = 1, 2, 4
+POL_AEG, POL_BELADY, POL_EVICT_ALL, POL_LRU, POL_LRU_PREFIX = 1, 2, 4, 8, 16
 INF = 0xFFFFFFFF
 COUNTERS = ["ACCESSES", "HITS", "MISSES", "MIG_HITS", "MIG_MISSES", "COMPULSORY", "INVALIDATED", "EVICTIONS",
             "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH", "INFEASIBLE_EPOCH",
@@ -212,7 +212,7 @@ class Oracle:
         cfg = replay_cfg(**(rcfg or {}))
         caps = np.ascontiguousarray(caps, np.uint32)
         nodes = np.arange(self.desc.n_nodes, dtype=np.uint32) if nodes is None else np.ascontiguousarray(nodes, np.uint32)
-        npol = bin(policy_mask & 7).count("1")
+        npol = bin(policy_mask & 31).count("1")
         out = np.zeros((npol, caps.size, self.desc.n_nodes, 16), np.int64)
         lib().oracle_replay_many(self.h, C.byref(cfg), policy_mask, caps.ctypes.data, caps.size, nodes.ctypes.data,
                                  nodes.size, out.ctypes.data, int(nthreads or os.cpu_count() or 1))

@@ -19,7 +19,9 @@
 //   aeg_key()       WA-LRU eq:eviction, eq:recency/eq:size, eq:reuse
 //                   (P:673-678), eq:overlap linear form, Alg. alg:ttl,
 //                   eq:pressure -- fp32 in the pinned order of DESIGN.md; also fp64
-//   replay()        epoch-synchronous replay R1-R4 for AEG, BELADY, EVICT_ALL
+//   replay()        epoch-synchronous replay R1-R4 for AEG, BELADY, EVICT_ALL and
+//                   the baselines of Table tab:competitive: LRU and LRU + Prefix
+//                   (DESIGN.md R-lru: recency = the block's latest position in the node stream)
 //   min_misses()    exact per-access Belady MIN without bypass
 // ============================================================================================
 #include <algorithm>
@@ -68,7 +70,7 @@ struct OPlace {
   uint64_t seed;
 };
 struct OReplay {
-  uint32_t policy;  // 1 AEG, 2 BELADY, 4 EVICT_ALL (one policy per call)
+  uint32_t policy;  // 1 AEG, 2 BELADY, 4 EVICT_ALL, 8 LRU, 16 LRU + Prefix (one policy per call)
   float alpha, beta, gamma;
   uint32_t p_low_pm, p_high_pm;
   int64_t ttl_max_us;
@@ -78,7 +80,7 @@ struct OReplay {
 namespace {
 
 const uint32_t INF = 0xFFFFFFFFu;
-enum { POL_AEG = 1, POL_BELADY = 2, POL_EVICT_ALL = 4 };
+enum { POL_AEG = 1, POL_BELADY = 2, POL_EVICT_ALL = 4, POL_LRU = 8, POL_LRU_PREFIX = 16 };
 // counter slots
 enum {
   C_ACCESSES, C_HITS, C_MISSES, C_MIG_HITS, C_MIG_MISSES, C_COMPULSORY, C_INVALIDATED, C_EVICTIONS,
@@ -539,6 +541,7 @@ struct Oracle {
     std::vector<uint8_t> res(nl, 0);
     std::vector<int64_t> tl(nl, 0);
     std::vector<uint32_t> nu(nl, INF);
+    std::vector<uint32_t> lp(nl, 0);  // latest position of each block in the node stream (LRU)
     std::set<uint32_t> S;
     for (int i = 0; i < C_N; ++i) ctr[i] = 0;
     uint64_t hash = 0;
@@ -588,6 +591,18 @@ struct Oracle {
           }
         } else if (cfg.policy == POL_BELADY) {
           for (uint32_t b : cand) keys.push_back({(uint64_t(nu[b]) << 32) | b, b});
+        } else if (cfg.policy == POL_LRU || cfg.policy == POL_LRU_PREFIX) {
+          // least recently used first: the smallest latest position has the largest key;
+          // LRU + Prefix keeps shared-prefix blocks until no private block is left (vLLM's
+          // prefix caching, the "LRU + Prefix" row of tab:competitive)
+          for (uint32_t b : cand) {
+            uint64_t key = (uint64_t(0xFFFFFFFFu - lp[b]) << 32) | b;
+            if (cfg.policy == POL_LRU_PREFIX) {
+              const bool priv = owner[nd.uniq[b]] < n_sessions;
+              key = (uint64_t(priv) << 63) | (uint64_t(0x7FFFFFFFu - lp[b]) << 32) | b;
+            }
+            keys.push_back({key, b});
+          }
         } else {
           for (uint32_t b : cand) keys.push_back({uint64_t(b), b});
         }
@@ -623,6 +638,7 @@ struct Oracle {
           }
           tl[b] = g.tval;
           nu[b] = nd.next_use[p];
+          lp[b] = uint32_t(p);
         }
       ctr[C_PEAK_RESIDENT] = std::max<int64_t>(ctr[C_PEAK_RESIDENT], int64_t(S.size()));
       ctr[C_EVENT_EPOCHS]++;
@@ -791,7 +807,7 @@ void oracle_replay_many(void* h, const OReplay* cfg, uint32_t policy_mask, const
                         const uint32_t* nodes_, uint32_t n_nodes_, int64_t* out, int nthreads) {
   Oracle* o = static_cast<Oracle*>(h);
   std::vector<uint32_t> pols;
-  for (uint32_t p : {1u, 2u, 4u}) if (policy_mask & p) pols.push_back(p);
+  for (uint32_t p : {1u, 2u, 4u, 8u, 16u}) if (policy_mask & p) pols.push_back(p);
   // next use per node first (parallel over nodes)
   {
     std::atomic<uint32_t> it{0};

@@ -39,8 +39,9 @@ namespace {
 
 constexpr int RT = 512;
 constexpr int RW = RT / 32;
-constexpr uint32_t KIND_MIG = 0x80000000u;
-constexpr uint32_t UMASK = 0x7FFFFFFFu;
+constexpr uint32_t KIND_MIG = 0x80000000u;  // u_of bit 31: the position is a MIG record
+constexpr uint32_t U_SHARED = 0x40000000u;  // u_of bit 30: the block is a shared-prefix block
+constexpr uint32_t UMASK = 0x3FFFFFFFu;
 constexpr int H1 = 4096;  // first-level key-part digit: [!prot:1 | q >> 10 : 11]
 
 // hierarchical bitmap; storage is allocated in whole c2 blocks (2^20 bits)
@@ -103,7 +104,7 @@ struct ReplayArgs {
   const uint32_t* items;  // packed (pi << 28) | (ci << 12) | node_list index, largest capacity first
   uint32_t n_items;
   const uint32_t* node_list;
-  uint32_t pol[3];
+  uint32_t pol[5];
   uint32_t n_caps;
   uint32_t n_nodes_total;
   int64_t* counters;
@@ -116,6 +117,7 @@ struct ReplayArgs {
   const CallKey* callkey;
   uint64_t o_res, o_nres, o_bits, o_c1, o_dbits, o_dc1, o_cnt, o_list0, o_list1, o_kbuf, o_vl, o_vu, o_ocall;
   uint32_t n2N_max, n2L_max;   // c2 entries of the two bitmaps (dynamic shared memory)
+  uint32_t n2R_max;            // c2 entries of the LRU bitmap (2N domain for LRU + Prefix)
   uint32_t dyn_c1;             // BELADY: the c1 arrays are in dynamic shared memory too
   uint32_t dyn_dbits_words;    // BELADY: dead bits in shared memory when n_local <= 32 * this
   uint32_t dyn_words;          // dynamic shared memory size in 32-bit words
@@ -456,19 +458,33 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
     const NodeArr nd = a.nodes[w];
     const bool belady = pol == SAGA_POLICY_BELADY;
     const bool aeg = pol == SAGA_POLICY_AEG;
+    const bool lru = pol == SAGA_POLICY_LRU || pol == SAGA_POLICY_LRU_PREFIX;
+    const bool pfx = pol == SAGA_POLICY_LRU_PREFIX;
+    const bool units = !belady && !lru;  // AEG / EVICT_ALL keep units and the live list
+    // LRU order: hierarchical bitmap over mirrored latest positions (oldest access = top bit);
+    // LRU + Prefix puts private blocks in the upper half so they go before any shared block
+    const uint64_t NM = pfx ? 2 * nd.N : nd.N;
+    auto lru_idx = [&](uint32_t p, bool shared) -> uint32_t {
+      return pfx && !shared ? (uint32_t)(2 * nd.N - 1 - p) : (uint32_t)(nd.N - 1 - p);
+    };
+    auto lru_pos = [&](uint32_t i) -> uint32_t {
+      return (uint32_t)(i >= nd.N ? 2 * nd.N - 1 - i : nd.N - 1 - i);
+    };
     const uint32_t n2N = max(1u, (uint32_t)((nd.N + (1u << 20) - 1) >> 20));
     const uint32_t n2L = max(1u, (nd.n_local + (1u << 20) - 1) >> 20);
     const uint32_t n1L = (nd.n_local + 1023u) >> 10;  // c1 blocks holding local ids
     // BELADY: c2 always in shared memory; c1 and the dead bits there too when they fit
     uint32_t* c2N = dyn;
     uint32_t* c2L = dyn + a.n2N_max;
-    const uint32_t c1off = (a.n2N_max + a.n2L_max + 3u) & ~3u;
+    const uint32_t c1off = (max(a.n2N_max + a.n2L_max, a.n2R_max) + 3u) & ~3u;
     uint32_t* c1N = a.dyn_c1 ? dyn + c1off : reinterpret_cast<uint32_t*>(base + a.o_c1);
     uint32_t* c1L = a.dyn_c1 ? c1N + a.n2N_max * 1024u : reinterpret_cast<uint32_t*>(base + a.o_dc1);
     const uint32_t dboff = a.dyn_c1 ? c1off + (a.n2N_max + a.n2L_max) * 1024u : c1off;
     uint32_t* dbits = (n1L * 32u <= a.dyn_dbits_words) ? dyn + dboff : reinterpret_cast<uint32_t*>(base + a.o_dbits);
     HB pend{reinterpret_cast<uint32_t*>(base + a.o_bits), c1N, c2N, n2N};
     HB dead{dbits, c1L, c2L, n2L};
+    const uint32_t n2R = max(1u, (uint32_t)((NM + (1u << 20) - 1) >> 20));
+    HB rec{reinterpret_cast<uint32_t*>(base + a.o_bits), reinterpret_cast<uint32_t*>(base + a.o_c1), dyn, n2R};
     // AEG / EVICT_ALL: newest-call table, then the unit counts, in shared memory when they fit
     uint32_t* ocall = a.ocall_smem ? dyn : reinterpret_cast<uint32_t*>(base + a.o_ocall);
     const uint32_t cnt_off = a.ocall_smem ? ((nd.n_lo + 3u) & ~3u) : 0u;
@@ -481,7 +497,13 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       uint4* b4 = reinterpret_cast<uint4*>(pend.bits);
       // whole 1024-bit blocks: the threshold search reads all 32 words of a block
       for (uint32_t i = threadIdx.x; i < (uint32_t)((nd.N + 1023) / 1024) * 8u; i += RT) b4[i] = zero;
-      if (belady) {
+      if (lru) {
+        for (uint32_t i = threadIdx.x; i < (uint32_t)((NM + 1023) / 1024) * 8u; i += RT) b4[i] = zero;
+        for (uint32_t i = threadIdx.x; i < n2R * 1024u; i += RT) rec.c1[i] = 0;
+        for (uint32_t i = threadIdx.x; i < n2R; i += RT) rec.c2[i] = 0;
+        uint4* n4 = reinterpret_cast<uint4*>(nres_a);
+        for (uint32_t i = threadIdx.x; i < (uint32_t)((nd.N + 1023) / 1024) * 8u; i += RT) n4[i] = zero;
+      } else if (belady) {
         for (uint32_t i = threadIdx.x; i < n2N * 1024u; i += RT) c1N[i] = 0;
         for (uint32_t i = threadIdx.x; i < n2L * 1024u; i += RT) c1L[i] = 0;
         for (uint32_t i = threadIdx.x; i < a.n2N_max + a.n2L_max; i += RT) dyn[i] = 0;
@@ -561,6 +583,10 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             const uint32_t q = nd.nxt[p];
             if (q == INF32) { hb_clear(dead, l); atomicSub(&sm.tot_dead, 1u); }
             else { hb_clear(pend, q); atomicSub(&sm.tot_pend, 1u); }
+          } else if (lru) {  // migrated-away blocks are private
+            hb_clear(rec, lru_idx(p, false));
+            const uint32_t q = nd.nxt[p];
+            if (q != INF32) atomicAnd(&nres_a[q >> 5], ~(1u << (q & 31)));
           } else {
             atomicAnd(&alive[p >> 5], ~(1u << (p & 31)));
             atomicSub(&cnt[nd.u_of[p] & UMASK], 1u);
@@ -611,7 +637,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
           lf[u] = in[u] ? P(0, pb) : 0u;
           uo[u] = in[u] ? P(1, pb) : 0u;
           pv[u] = (in[u] && !belady) ? P(3, pb) : 0u;
-          up[u] = (in[u] && !belady) ? P(4, pb) : 0u;
+          up[u] = (in[u] && units) ? P(4, pb) : 0u;
           nw[u] = wbu < P1 ? nres[wbu >> 5] : 0u;
         }
 #pragma unroll
@@ -636,9 +662,11 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             atomicAnd(&nres[wbu >> 5], ~rm);
             if (belady) { atomicSub(&pend.c1[wbu >> 10], (uint32_t)__popc(rm)); atomicSub(&pend.c2[wbu >> 20], (uint32_t)__popc(rm)); }
           }
-          if (!belady) {
+          if (units) {
             warp_bits(alive, resident, pv[u], false);
             warp_count(cnt, resident, up[u], false);
+          } else if (lru) {
+            hb_update_warp(rec, resident, lru_idx(pv[u], (uo[u] & U_SHARED) != 0), false);
           }
         }
       }
@@ -677,6 +705,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             sm.tot_dead = nd_ - min(k, nd_);
             sm.tot_pend = np_ - (k > nd_ ? k - nd_ : 0u);
           }
+        } else if (lru) {
+          // every resident non-in-flight block has one bit; k <= |cand| because |A| <= C
+          hb_take_top(rec, k, vlist, 0u, sm, a.dbg);
         } else {
           ListRec* L = lists[cur];
           // whole-unit eviction: list every resident latest position of unit u (warp-collective)
@@ -864,7 +895,8 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
         if (threadIdx.x == 0 && nvl > k) dbg_fail(a.dbg, __LINE__, nvl, k, pol);
         for (uint32_t i = threadIdx.x; i < ((nvl + 31) & ~31u); i += RT) {
           const bool in = i < nvl;
-          const uint32_t x = in ? vlist[i] : 0u;
+          uint32_t x = in ? vlist[i] : 0u;
+          if (lru && in) x = lru_pos(x);  // LRU lists bitmap indices of mirrored positions
           const uint32_t lid = (x & VT_LID) ? (x & ~VT_LID) : (in ? nd.lidf[x] & LID_MASK : 0u);
           if (!belady) {  // a victim's next use is no longer resident
             const uint32_t qn = in ? nd.nxt[x] : INF32;
@@ -913,6 +945,9 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             const uint32_t md = __ballot_sync(0xffffffffu, last[u] && q[u] == INF32);
             const uint32_t mp = __ballot_sync(0xffffffffu, last[u] && q[u] != INF32);
             if (lane == 0 && (md | mp)) { atomicAdd(&sm.tot_dead, __popc(md)); atomicAdd(&sm.tot_pend, __popc(mp)); }
+          } else if (lru) {
+            hb_update_warp(rec, last[u], lru_idx((uint32_t)pb, (uo[u] & U_SHARED) != 0), true);
+            warp_bits(nres_a, last[u] && q[u] != INF32, q[u], true);
           } else {
             const uint32_t wv = __ballot_sync(0xffffffffu, last[u]);
             if (lane == 0 && wv) atomicOr(&alive[(wb + (uint64_t)u * RT) >> 5], wv);
@@ -925,7 +960,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
       S += nnew;
       PH(6);
       // ---- live unit list: keep units with cnt > 0, append this epoch's units ----
-      if (!belady) {
+      if (units) {
         __syncthreads();
         const ListRec* L = lists[cur];
         ListRec* L2 = lists[cur ^ 1];
@@ -1068,10 +1103,11 @@ __global__ void k_unit_end(const uint32_t* u_pos, uint32_t n_units, uint64_t N, 
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += gridDim.x * blockDim.x)
     urec[u].pe = u + 1 < n_units ? u_pos[u + 1] : (uint32_t)N;
 }
-__global__ void k_unit_of(const uint32_t* hpos, uint64_t N, const uint32_t* u_kind, uint32_t* u_of) {
+__global__ void k_unit_of(const uint32_t* hpos, uint64_t N, const uint32_t* u_kind, const UnitRec* urec,
+                          uint32_t* u_of) {
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = hpos[p + 1] - 1;
-    u_of[p] = u | (u_kind[u] ? KIND_MIG : 0u);
+    u_of[p] = u | (u_kind[u] ? KIND_MIG : 0u) | ((urec[u].lo & LO_SHARED) ? U_SHARED : 0u);
   }
 }
 __global__ void k_ev_index(TraceView v, const uint64_t* ev_pos, const uint32_t* ev_e, uint32_t J, const uint32_t* hpos,
@@ -1167,7 +1203,7 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
     k_unit_fill<<<grid_for(N), NTHREADS, 0, s>>>(head, hpos, N, nd.lidf, nd.lown, nd.g_pos, nd.G, nd.g_t, nd.g_kind, s2lo,
                                                  v.n_sessions, u_pos, ur, u_kind);
     k_unit_end<<<grid_for(nu), NTHREADS, 0, s>>>(u_pos, nu, N, ur);
-    k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(hpos, N, u_kind, nd.u_of);
+    k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(hpos, N, u_kind, ur, nd.u_of);
     k_prev_unit<<<grid_for(N), NTHREADS, 0, s>>>(nd.prv, nd.u_of, N, nd.upu);
     k_unit_mono<<<grid_for(N), NTHREADS, 0, s>>>(nd.lidf, nd.u_of, N, ur);
     count_launch(5);
@@ -1191,8 +1227,8 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
 saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                        const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s) {
   const TraceView& v = t->v;
-  uint32_t pol[3], n_pol = 0;
-  for (uint32_t p : {1u, 2u, 4u}) if (cfg->policy_mask & p) pol[n_pol++] = p;
+  uint32_t pol[5], n_pol = 0;
+  for (uint32_t p : {1u, 2u, 4u, 8u, 16u}) if (cfg->policy_mask & p) pol[n_pol++] = p;
   if (n_pol == 0 || n_caps == 0 || n_owned == 0) return SAGA_OK;
   if (n_caps > 0xFFFFu || n_owned > 0xFFFu) { set_error("saga_replay: at most 65535 capacities and 4095 nodes per call"); return SAGA_ERR_INVALID_ARG; }
   uint32_t cap_max = 0;
@@ -1240,12 +1276,19 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
   const uint64_t n2N = std::max<uint64_t>(1, (maxN + (1u << 20) - 1) >> 20);
   const uint64_t n2L = std::max<uint64_t>(1, (max_local + (1u << 20) - 1) >> 20);
+  const bool any_pfx = (cfg->policy_mask & SAGA_POLICY_LRU_PREFIX) != 0;
+  if (any_pfx && 2 * maxN >= (1ull << 31)) {
+    set_error("saga_replay: LRU + Prefix needs node streams below 2^30 accesses");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  const uint64_t n2R = std::max<uint64_t>(1, ((any_pfx ? 2 * maxN : maxN) + (1u << 20) - 1) >> 20);
+  const uint64_t n2B = std::max(n2N, n2R);  // the position bitmap serves BELADY, AEG and LRU
   ReplayArgs a{};
   uint64_t off = 0;
   a.o_res = off; off += al(max_local * 4 + 16);
   a.o_nres = off; off += al(n2N * 32768 * 4);
-  a.o_bits = off; off += al(n2N * 32768 * 4);
-  a.o_c1 = off; off += al(n2N * 1024 * 4);
+  a.o_bits = off; off += al(n2B * 32768 * 4);
+  a.o_c1 = off; off += al(n2B * 1024 * 4);
   a.o_dbits = off; off += al(n2L * 32768 * 4);
   a.o_dc1 = off; off += al(n2L * 1024 * 4);
   a.o_cnt = off; off += al(max_units * 4);
@@ -1263,10 +1306,10 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   uint64_t dyn_max = 64ull * 1024;
   if (const char* e = getenv("SAGA_REPLAY_SMEM_KB")) dyn_max = std::max<uint64_t>(1, strtoull(e, nullptr, 10)) * 1024;
   dyn_max = std::min<uint64_t>(dyn_max, 200ull * 1024);
-  const uint64_t c2_bytes = ((n2N + n2L + 3) & ~3ull) * 4;
+  const uint64_t c2_bytes = ((std::max(n2N + n2L, n2R) + 3) & ~3ull) * 4;
   const uint64_t c1_bytes = (n2N + n2L) * 1024 * 4;
   const uint64_t db_bytes = ((max_local + 1023) >> 10) * 32 * 4;
-  a.n2N_max = (uint32_t)n2N; a.n2L_max = (uint32_t)n2L;
+  a.n2N_max = (uint32_t)n2N; a.n2L_max = (uint32_t)n2L; a.n2R_max = (uint32_t)n2R;
   a.dyn_c1 = (c2_bytes + c1_bytes <= dyn_max) ? 1u : 0u;
   uint64_t dyn_b = a.dyn_c1 ? c2_bytes + c1_bytes : c2_bytes;
   if (dyn_b + db_bytes <= dyn_max) { a.dyn_dbits_words = (uint32_t)(db_bytes / 4); dyn_b += db_bytes; }
@@ -1312,7 +1355,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   SAGA_CK(cudaMemsetAsync(work, 0, 32, s));
   a.v = v;
   a.nodes = d_nodes; a.caps = d_caps; a.items = d_items; a.n_items = n_items; a.node_list = d_list;
-  a.pol[0] = pol[0]; a.pol[1] = n_pol > 1 ? pol[1] : 0; a.pol[2] = n_pol > 2 ? pol[2] : 0;
+  for (uint32_t i = 0; i < 5; ++i) a.pol[i] = i < n_pol ? pol[i] : 0u;
   a.n_caps = n_caps; a.n_nodes_total = t->n_nodes; a.counters = counters;
   a.alpha = cfg->alpha; a.beta = cfg->beta; a.gamma = cfg->gamma;
   a.p_low = cfg->p_low_pm; a.p_high = cfg->p_high_pm; a.ttl_max = cfg->ttl_max_us;

@@ -366,7 +366,7 @@ saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream) {
   CHECK_HANDLE(t);
   if (!cfg || (n_caps && !caps) || (n_owned && !nodes) || !counters_dev) { set_error("saga_replay: NULL argument"); return SAGA_ERR_INVALID_ARG; }
-  if ((cfg->policy_mask & ~7u) || !(cfg->policy_mask & 7u)) { set_error("saga_replay: bad policy_mask"); return SAGA_ERR_INVALID_ARG; }
+  if ((cfg->policy_mask & ~31u) || !(cfg->policy_mask & 31u)) { set_error("saga_replay: bad policy_mask"); return SAGA_ERR_INVALID_ARG; }
   if (cfg->p_high_pm <= cfg->p_low_pm || cfg->p_high_pm > 1000) { set_error("saga_replay: need p_low_pm < p_high_pm <= 1000"); return SAGA_ERR_INVALID_ARG; }
   for (uint32_t i = 0; i < n_caps; ++i)
     if (caps[i] == 0 || caps[i] > (1u << 28)) { set_error("saga_replay: capacity %u out of range (1..2^28)", caps[i]); return SAGA_ERR_CAPACITY; }

@@ -39,7 +39,7 @@ def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, wo
         t.stream.synchronize()
         wlo, whi = (int(x) for x in rng.cpu())
     caps = caps_fn(wlo, whi)
-    npol = bin(replay_cfg.get("policy_mask", 3) & 7).count("1")
+    npol = bin(replay_cfg.get("policy_mask", 3) & 31).count("1")
     if counters is None:
         counters = torch.zeros((npol, len(caps), desc.n_nodes, saga.NCOUNT), dtype=torch.int64,
                                device=f"cuda:{device}")

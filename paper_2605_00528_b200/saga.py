@@ -14,7 +14,7 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libsaga.so")
 
-POLICY_AEG, POLICY_BELADY, POLICY_EVICT_ALL = 1, 2, 4
+POLICY_AEG, POLICY_BELADY, POLICY_EVICT_ALL, POLICY_LRU, POLICY_LRU_PREFIX = 1, 2, 4, 8, 16
 NCOUNT = 16
 COUNTERS = ["ACCESSES", "HITS", "MISSES", "MIG_HITS", "MIG_MISSES", "COMPULSORY", "INVALIDATED", "EVICTIONS",
             "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH", "INFEASIBLE_EPOCH",

@@ -109,12 +109,13 @@ def _caps_for(o, d, name):
 def test_replay_counters_equal(pair):
     name, d, pc, o, t = pair
     caps = _caps_for(o, d, name)
-    ref = o.replay_many(7, caps)
-    got = torch.zeros((3, len(caps), d.n_nodes, 16), dtype=torch.int64, device="cuda")
-    t.replay(dict(policy_mask=7), caps, list(range(d.n_nodes)), got)
+    # AEG, BELADY, EVICT_ALL and the tab:competitive baselines LRU, LRU + Prefix
+    ref = o.replay_many(31, caps)
+    got = torch.zeros((5, len(caps), d.n_nodes, 16), dtype=torch.int64, device="cuda")
+    t.replay(dict(policy_mask=31), caps, list(range(d.n_nodes)), got)
     torch.cuda.synchronize()
     g = got.cpu().numpy()
-    for pi in range(3):
+    for pi in range(5):
         for ci in range(len(caps)):
             for w in range(d.n_nodes):
                 assert np.array_equal(g[pi, ci, w], ref[pi, ci, w]), (name, pi, caps[ci], w, g[pi, ci, w], ref[pi, ci, w])

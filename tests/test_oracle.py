@@ -186,6 +186,62 @@ def test_min_bruteforce_random(O):
 
 
 # ------------------------------------------------------------------------------------------
+# LRU / LRU + Prefix baselines (Table tab:competitive; DESIGN.md R-lru): with one
+# access per epoch the epoch-batched replay is per-access paging, which must equal a textbook
+# LRU simulation (ordered dictionary) -- victims, in order, and misses.
+# ------------------------------------------------------------------------------------------
+
+def _textbook_lru(seq, C, shared=0):
+    """Per-access LRU without bypass; with `shared` > 0 blocks < shared are evicted only when no
+    other block is resident (prefix caching)."""
+    from collections import OrderedDict
+    cache, miss, victims = OrderedDict(), 0, []
+    for b in seq:
+        if b in cache:
+            cache.move_to_end(b)
+            continue
+        miss += 1
+        if len(cache) == C:
+            priv = [x for x in cache if x >= shared]
+            v = priv[0] if priv else next(iter(cache))
+            del cache[v]
+            victims.append(v)
+        cache[b] = True
+    return miss, victims
+
+
+@pytest.mark.parametrize("n_shared", [0, 2])
+def test_lru_equals_textbook(O, n_shared):
+    rng = np.random.default_rng(21 + n_shared)
+    for _ in range(300):
+        nb = int(rng.integers(n_shared + 2, n_shared + 8))
+        n = int(rng.integers(1, 25))
+        seq = [int(x) for x in rng.integers(0, nb, size=n)]
+        o = O.Oracle(make_stream_trace(seq, n_shared=n_shared), default_place_cfg())
+        lid = o.next_use(0)["local_id"]
+        g2l = {int(b): int(l) for b, l in zip(o.stream(0)["block"], lid)}
+        for C in range(1, 6):
+            for pol, shared in ((O.POL_LRU, 0), (O.POL_LRU_PREFIX, n_shared)):
+                m, vic = _textbook_lru(seq, C, shared)
+                ctr, log = o.replay(pol, 0, C, log=True)
+                assert misses(ctr, O) == m, (seq, C, pol)
+                assert [int(x) for x in log] == [g2l[v] for v in vic], (seq, C, pol)
+
+
+def test_lru_bounded_by_belady_epoch(O):
+    for seed in range(6):
+        d = make_random_small(seed, n_sessions=6, n_nodes=2, max_calls=5, max_blocks=8)
+        o = O.Oracle(d, default_place_cfg(seed))
+        for w in range(d.n_nodes):
+            lo, hi = o.sweep_range(w)
+            for C in range(max(lo, 1), hi + 3):
+                b = o.replay(O.POL_BELADY, w, C)
+                for pol in (O.POL_LRU, O.POL_LRU_PREFIX):
+                    r = o.replay(pol, w, C)
+                    assert hits(r, O) <= hits(b, O), (seed, w, C, pol)
+
+
+# ------------------------------------------------------------------------------------------
 # BELADY-epoch = brute-force optimum over epoch-batched policies (incl. invalidations)
 # ------------------------------------------------------------------------------------------
 
