@@ -427,8 +427,9 @@ def main():
                 "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
 
     bulk = None
-    if rank == 0 and not args.no_bulk:
-        t_b, _, _ = step(dd)
+    if world == 1 and not args.no_bulk:  # single process: no collective may be issued by one rank
+        with torch.cuda.stream(stream):
+            t_b, _, _ = pipeline.run_step(desc, pc, rcfg, caps_fn, device=local, stream=stream, host=dd)
         stream.synchronize()
         bulk = bulk_score_select(t_b, desc, stream, dev)
         t_b.free()
