@@ -249,6 +249,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-bulk", action="store_true")
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
+    ap.add_argument("--policy-mask", type=int, default=3,
+                    help="1 AEG, 2 BELADY, 4 EVICT_ALL, 8 LRU, 16 LRU+Prefix (default 3: the metric's pair)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -276,7 +278,7 @@ def main():
         seed = inspect.signature(CONFIGS[args.config]).parameters["seed"].default + 1000 * rank
     desc = make(args.config, n_sessions=args.n_sessions, seed=seed)
     pc = place_cfg_for(desc)
-    rcfg = dict(policy_mask=3)
+    rcfg = dict(policy_mask=args.policy_mask)
     caps_fn = sweep_for(args.config)
     shard_caps = (not trials) and desc.n_nodes == 1 and world > 1
     comm = saga.Comm(rank, world, local) if world > 1 else None
@@ -326,7 +328,7 @@ def main():
     mine = (list(range(desc.n_nodes)) if trials else pipeline.owned_nodes(desc.n_nodes, rank, world)) \
         if not shard_caps else [0]
     n_acc_local = sum(t.info(w)[0] for w in mine)
-    n_pol = 2
+    n_pol = bin(args.policy_mask & 31).count("1")
     if shard_caps:
         n_caps_local = len([i for i in range(len(caps)) if i % world == rank])
         rep_local = n_acc_local * n_pol * n_caps_local
@@ -448,7 +450,8 @@ def main():
             "vs_baseline": None,
             "dtype": "int64/fp32", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "trace": desc.name,
-                       "nodes": desc.n_nodes, "caps": caps, "policies": ["AEG", "BELADY"],
+                       "nodes": desc.n_nodes, "caps": caps, "policies": [nm for b, nm in ((1, "AEG"), (2, "BELADY"), (4, "EVICT_ALL"), (8, "LRU"),
+                                                                  (16, "LRU_PREFIX")) if args.policy_mask & b],
                        "trace_accesses": n_access, "access_replays_per_step": replay_accesses,
                        "trace_accesses_per_s": n_access / (ms / 1e3),
                        "l2": "inputs larger than L2 (node streams 4 B/access + per-node next-use arrays)",

@@ -42,7 +42,9 @@ constexpr int RW = RT / 32;
 constexpr uint32_t KIND_MIG = 0x80000000u;  // u_of bit 31: the position is a MIG record
 constexpr uint32_t U_SHARED = 0x40000000u;  // u_of bit 30: the block is a shared-prefix block
 constexpr uint32_t UMASK = 0x3FFFFFFFu;
-constexpr int H1 = 4096;  // first-level key-part digit: [!prot:1 | q >> 10 : 11]
+// first-level key-part digit: !prot * 1025 + (q >> 10), q <= 2^20 (2050 values, kp order)
+constexpr int H1 = 2560;
+__device__ __forceinline__ uint32_t kp_digit(uint32_t kp) { return (kp >> 31) * 1025u + ((kp & 0x1FFFFFu) >> 10); }
 
 // hierarchical bitmap; storage is allocated in whole c2 blocks (2^20 bits)
 struct HB {
@@ -763,7 +765,7 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
                 const OwnerKeyIn oi = owner_in(v, ck, ocall, r.lo, act);
                 const uint32_t q = quantize_q20(wa_lru_score(x, r.t, oi.size, oi.P));
                 kp = ((uint32_t)!ttl_protected(x, oi) << 31) | q;
-                atomicAdd(&sm.hist[((kp >> 31) << 11) | (q >> 10)], c);
+                atomicAdd(&sm.hist[kp_digit(kp)], c);
               }
               L[i].kp = kp;
             }
@@ -774,13 +776,14 @@ __global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
               const uint32_t kp = L[i].kp;
-              if ((((kp >> 31) << 11) | ((kp & 0x1FFFFFu) >> 10)) != d1) continue;
+              if (kp_digit(kp) != d1) continue;
               const uint32_t c = cnt[L[i].u];
               if (c) atomicAdd(&sm.hist[kp & 1023u], c);
             }
             __syncthreads();
             find_level<1024 / RT>(sm.hist, 0, 1024, r1, d2, r2, sm, par);
-            const uint32_t kps = ((d1 >> 11) << 31) | ((d1 & 2047u) << 10) | d2;
+            const uint32_t pb1 = d1 >= 1025u ? 1u : 0u;
+            const uint32_t kps = (pb1 << 31) | ((d1 - pb1 * 1025u) << 10) | d2;
             const bool prot_piv = !(kps >> 31);
             const bool whole = sm.hist[d2] == r2;  // the pivot units are evicted whole
             if (threadIdx.x == 0) { sm.n_piv = 0; sm.n_vu = 0; sm.n_pu = 0; }
