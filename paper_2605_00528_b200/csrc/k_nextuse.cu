@@ -72,24 +72,31 @@ __global__ void __launch_bounds__(SS_T) k_segscan(const uint32_t* __restrict__ s
   uint32_t wpre = 0, tot = 0;
   for (int w = 0; w < SS_T / 32; ++w) { if (w < wid) wpre += wsum[w]; tot += wsum[w]; }
   const uint32_t texcl = wpre + x - heads;
-  // look-back on the tile total
-  if (threadIdx.x == 0) {
+  // decoupled look-back on the tile total, 32 predecessors per step (lane l reads tile t2 - l)
+  if (wid == 0) {
     unsigned long long* my = status + tile;
     unsigned long long ex = 0;
-    if (tile == 0) st_relaxed64(my, F_INC | tot);
-    else {
-      st_relaxed64(my, F_AGG | tot);
+    if (tile == 0) {
+      if (lane == 0) st_relaxed64(my, F_INC | tot);
+    } else {
+      if (lane == 0) st_relaxed64(my, F_AGG | tot);
       int64_t t2 = (int64_t)tile - 1;
       while (true) {
-        unsigned long long s;
-        do { s = ld_relaxed64(status + t2); } while ((s & (F_AGG | F_INC)) == 0);
-        ex += s & V_MASK;
-        if (s & F_INC) break;
-        --t2;
+        const int64_t idx = t2 - lane;
+        unsigned long long s = F_INC;  // before tile 0: an inclusive zero
+        if (idx >= 0) { do { s = ld_relaxed64(status + idx); } while ((s & (F_AGG | F_INC)) == 0); }
+        const uint32_t inc = __ballot_sync(0xffffffffu, (s & F_INC) != 0);
+        const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive predecessor, else all 32
+        unsigned long long v = lane <= stop ? (s & V_MASK) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        ex += v;
+        if (inc) break;
+        t2 -= 32;
       }
-      st_relaxed64(my, F_INC | (ex + tot));
+      if (lane == 0) st_relaxed64(my, F_INC | (ex + tot));
     }
-    s_prefix = ex;
+    if (lane == 0) s_prefix = ex;
   }
   __syncthreads();
   uint32_t lid = (uint32_t)(s_prefix + texcl);  // number of heads before this thread's first item
