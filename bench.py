@@ -31,6 +31,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# steps in flight use one stream each; with the default 8 hardware work queues two of torch's pool
+# streams can share a queue, which serialises one step's kernels behind the other's placement
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "trace accesses/sec (AEG score+evict+replay, Bélády); HBM GB/s vs B200 peak"
 UNIT = "access-replays/s"
@@ -249,6 +252,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-bulk", action="store_true")
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
+    ap.add_argument("--inflight", type=int, default=None,
+                    help="independent steps in flight on separate streams (default 2; 1 for C4/C5)")
     ap.add_argument("--policy-mask", type=int, default=3,
                     help="1 AEG, 2 BELADY, 4 EVICT_ALL, 8 LRU, 16 LRU+Prefix (default 3: the metric's pair)")
     args = ap.parse_args()
@@ -281,9 +286,13 @@ def main():
     rcfg = dict(policy_mask=args.policy_mask)
     caps_fn = sweep_for(args.config)
     shard_caps = (not trials) and desc.n_nodes == 1 and world > 1
-    comm = saga.Comm(rank, world, local) if world > 1 else None
-    p_rank, p_world, p_comm = (0, 1, None) if trials else (rank, world, comm)
-    stream = torch.cuda.Stream(device=dev)
+    inflight = max(1, args.inflight or (2 if desc.n_calls < 1_000_000 else 1))
+    # one stream, trace handle and communicator per in-flight step (see run_steps)
+    comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
+    comm = comms[0]
+    p_rank, p_world = (0, 1) if trials else (rank, world)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(inflight)]
+    stream = streams[0]
     host_pinned = saga.HostDesc(desc, pinned=True)
     # device-resident descriptor for `value` (the library deep-copies it device-to-device)
     dev_keep = []
@@ -300,28 +309,104 @@ def main():
     dd.keep = dev_keep
     dd.c = saga.TraceDescC(desc.n_calls, desc.n_sessions, desc.n_types, desc.n_aeg_nodes, desc.n_edges, desc.n_ranges,
                            desc.n_blocks, desc.n_nodes, desc.block_tokens, *dptrs)
-    counters = None
+    counters = [None] * inflight
+    import threading
+    order = {"cv": threading.Condition(), "done": {}}
+    timeline = [] if os.environ.get("SAGA_TIMELINE") else None
 
-    def step(host):
-        nonlocal counters
-        with torch.cuda.stream(stream):
-            t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=p_rank, world=p_world, comm=p_comm,
-                                             device=local, stream=stream, host=host, counters=counters,
-                                             shard_caps=shard_caps)
-            if trials and comm is not None:  # A8: combine the per-trial counters over ranks
-                comm.allreduce(ctr, op=0, stream=t.stream)
-        counters = ctr
+    def mark(st, what, j):  # SAGA_TIMELINE=1: device-side timeline of the steps, printed to stderr
+        if timeline is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(st)
+            timeline.append((what, j, e, time.perf_counter()))
+
+    def step(host, i=0, j=None):
+        """One step on stream i.  With steps in flight (j = step index), step j's expansion,
+        next use and replay start on the device after step j-1's replay, while its placement (a
+        single warp on one SM) runs beside that replay.  Every step does all of its work."""
+        s_ = streams[i]
+        before = after = None
+        if j is not None and inflight > 1:
+            def before(st):
+                if j == 0:
+                    return
+                with order["cv"]:
+                    order["cv"].wait_for(lambda: (j - 1) in order["done"])
+                    ev = order["done"][j - 1]
+                mark(st, "placed", j)
+                st.wait_event(ev)
+                mark(st, "go", j)
+
+            def after(st):
+                mark(st, "replayed", j)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                with order["cv"]:
+                    order["done"][j] = ev
+                    order["cv"].notify_all()
+        mark(s_, "start", j)
+        with torch.cuda.stream(s_):
+            t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=p_rank, world=p_world,
+                                             comm=None if trials else comms[i], device=local, stream=s_, host=host,
+                                             counters=counters[i], shard_caps=shard_caps,
+                                             before_expand=before, after_replay=after,
+                                             mark=(lambda st, w: mark(st, w, j)) if timeline is not None else None)
+            if trials and comms[i] is not None:  # A8: combine the per-trial counters over ranks
+                comms[i].allreduce(ctr, op=0, stream=t.stream)
+        counters[i] = ctr
         return t, caps, ctr
+
+    def run_steps(k, host, d2h=None):
+        """k steps, step j on stream j mod inflight (one host thread per stream).  Device-timed:
+        every stream starts after ev0 on streams[0], which waits for all of them before ev1.
+        Returns (ms per step, (caps, counters) of the last step on stream 0)."""
+        import concurrent.futures as cf
+        with order["cv"]:
+            order["done"] = {}
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(streams[0])
+        order["h0"] = time.perf_counter()
+        for s_ in streams[1:]:
+            s_.wait_event(ev0)
+
+        def worker(i):
+            torch.cuda.set_device(local)
+            last = None
+            for j in range(i, k, inflight):
+                t, caps, ctr = step(host, i, j)
+                if d2h is not None:
+                    d2h(i, ctr)
+                t.free()
+                last = (caps, ctr)
+            return last
+
+        if inflight == 1:
+            outs = [worker(0)]
+        else:
+            with cf.ThreadPoolExecutor(inflight) as ex:
+                outs = list(ex.map(worker, range(inflight)))
+        for s_ in streams[1:]:
+            e = torch.cuda.Event()
+            e.record(s_)
+            streams[0].wait_event(e)
+        ev1.record(streams[0])
+        torch.cuda.synchronize()
+        if timeline:
+            for what, j, e, h in timeline:
+                print(f"timeline step {j} {what:9s} dev {ev0.elapsed_time(e):9.2f} ms  host {1e3 * (h - order['h0']):9.2f} ms",
+                      file=sys.stderr)
+            timeline.clear()
+        return ev0.elapsed_time(ev1) / k, outs[0]
 
     def barrier():
         if world > 1:
             dist.barrier(device_ids=[local])
 
     # ---- warm-up ----
-    for _ in range(args.warmup):
-        t, caps, _ = step(dd)
-        t.free()
-    torch.cuda.synchronize()
+    run_steps(max(args.warmup, inflight), dd)
+    # latency of one step alone (nothing else in flight)
+    lat_ms, _ = run_steps(1, dd)
     # per-step work (access-replays over all ranks)
     t, caps, ctr = step(dd)
     stream.synchronize()
@@ -348,17 +433,9 @@ def main():
     l0 = saga.kernel_launches()
     barrier()
     torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        t, caps, ctr = step(dd)
-        t.free()
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    ms, (caps, ctr) = run_steps(args.steps, dd)
     barrier()
     launches = saga.kernel_launches() - l0
-    ms = ev0.elapsed_time(ev1) / args.steps
     import ctypes as C
     pm = (C.c_double * 9)()
     pn = (C.c_uint64 * 9)()
@@ -377,28 +454,23 @@ def main():
     if not args.no_e2e:
         barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        out_host = torch.empty(tuple(ctr.shape), dtype=torch.int64, pin_memory=True)
-        for _ in range(args.steps):
-            t, caps, c2 = step(host_pinned)
-            with torch.cuda.stream(stream):
-                out_host.copy_(c2, non_blocking=True)
-            stream.synchronize()
-            t.free()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        out_host = [torch.empty(tuple(ctr.shape), dtype=torch.int64, pin_memory=True) for _ in range(inflight)]
+
+        def d2h(i, c2):  # the step's result back to the host, inside the timed region
+            with torch.cuda.stream(streams[i]):
+                out_host[i].copy_(c2, non_blocking=True)
+            streams[i].synchronize()
+
+        ems, _ = run_steps(args.steps, host_pinned, d2h=d2h)
         barrier()
-        ems = e0.elapsed_time(e1) / args.steps
         et = torch.tensor([ems], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         ems = float(et[0])
         e2e = {"value": replay_accesses / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": host_pinned.nbytes,
-               "d2h_bytes_per_step": int(out_host.numel() * 8), "ms_per_step": ems}
-        assert np.array_equal(out_host.numpy(), counters_host), "e2e counters differ from the device-resident run"
+               "d2h_bytes_per_step": int(out_host[0].numel() * 8), "ms_per_step": ems}
+        for oh in out_host:
+            assert np.array_equal(oh.numpy(), counters_host), "e2e counters differ from the device-resident run"
 
     # ---- roofline of the dominant kernel family (per-launch, CUDA events on the launching stream) ----
     peak, peak_kind = hbm_peak()
@@ -455,6 +527,7 @@ def main():
                        "trace_accesses": n_access, "access_replays_per_step": replay_accesses,
                        "trace_accesses_per_s": n_access / (ms / 1e3),
                        "l2": "inputs larger than L2 (node streams 4 B/access + per-node next-use arrays)",
+                       "steps_in_flight": inflight, "step_latency_ms": lat_ms,
                        "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
                                     else ("capacity points" if shard_caps else "cache nodes w mod R"))},
             "e2e": e2e, "gpu_launches": int(launches),
@@ -462,8 +535,9 @@ def main():
             "counters_checksum": int(np.bitwise_xor.reduce(counters_host.reshape(-1).view(np.uint64))),
         }
         print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.destroy()
+    for c_ in comms:
+        if c_ is not None:
+            c_.destroy()
     if world > 1:
         dist.destroy_process_group()
 

@@ -176,6 +176,15 @@ const char* saga_last_error(void);
 saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask,
                             int device, saga_stream_t stream, saga_trace** out);
 
+/* saga_load_trace with flags.  SAGA_LOAD_DEFER_EXPAND: return after validation and placement
+ * (still syncs); each owned node's stream (A3) is expanded on the handle's stream by the first
+ * call that needs it (saga_trace_info, saga_node_stream*, saga_belady_next_use).  Lets a caller
+ * with several traces in flight run one trace's single-SM placement beside another's replay and
+ * start the SM-hungry expansion / next-use only when that replay is done (stream-ordered). */
+enum { SAGA_LOAD_DEFER_EXPAND = 1 };
+saga_status saga_load_trace_ex(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask,
+                               int device, saga_stream_t stream, uint32_t flags, saga_trace** out);
+
 /* Sizes of node `node`'s stream: accesses and (after saga_belady_next_use) distinct blocks
  * (UINT32_MAX before).  Syncs.  SAGA_ERR_STATE if the node is not owned. */
 saga_status saga_trace_info(const saga_trace* t, uint32_t node, uint64_t* n_access, uint32_t* n_local_blocks);

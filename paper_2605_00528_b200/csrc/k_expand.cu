@@ -172,11 +172,11 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
     k_scatter_mig<<<grid_for(nm), NTHREADS, 0, s>>>(t->migs, ft, pt, nm, mlist);
     k_scatter_mig<<<grid_for(nm), NTHREADS, 0, s>>>(t->migs, fv, pv, nm, ilist);
     count_launch(2);
-    SAGA_CK(cudaMemcpyAsync(&nM, pt + nm, 4, cudaMemcpyDeviceToHost, s));
-    SAGA_CK(cudaMemcpyAsync(&nI, pv + nm, 4, cudaMemcpyDeviceToHost, s));
+    SAGA_CK(d2h(&nM, pt + nm, 4, s));
+    SAGA_CK(d2h(&nI, pv + nm, 4, s));
   }
-  SAGA_CK(cudaMemcpyAsync(&nC, pos + nc, 4, cudaMemcpyDeviceToHost, s));
   SAGA_CK_LAUNCH();
+  SAGA_CK(d2h(&nC, pos + nc, 4, s));
   SAGA_CK(cudaStreamSynchronize(s));
   const uint32_t G = nC + nM;
   nd.G = G;
@@ -202,9 +202,9 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
   SAGA_CK(scan_u32(t, head, hpos, G));
   uint32_t Jr = 0;
   uint64_t N = 0;
-  SAGA_CK(cudaMemcpyAsync(&Jr, hpos + G, 4, cudaMemcpyDeviceToHost, s));
-  SAGA_CK(cudaMemcpyAsync(&N, nd.g_pos + G, 8, cudaMemcpyDeviceToHost, s));
   SAGA_CK_LAUNCH();
+  SAGA_CK(d2h(&Jr, hpos + G, 4, s));
+  SAGA_CK(d2h(&N, nd.g_pos + G, 8, s));
   SAGA_CK(cudaStreamSynchronize(s));
   if (N >= (1ull << 31)) { set_error("node %u stream has %llu accesses (limit 2^31)", w, (unsigned long long)N); return SAGA_ERR_STATE; }
   nd.N = N;

@@ -224,7 +224,7 @@ saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d) {
   uint32_t* owner = dalloc<uint32_t>(t, d->n_blocks);
   if (!err || !owner) { set_error("saga_load_trace: out of device memory"); return SAGA_ERR_OOM; }
   VErr init{0u, 0xFFFFFFFFu};
-  SAGA_CK(cudaMemcpyAsync(err, &init, sizeof(VErr), cudaMemcpyHostToDevice, t->stream));
+  SAGA_CK(h2d(err, &init, sizeof(VErr), t->stream));
   SAGA_CK(cudaMemsetAsync(owner, 0xFF, size_t(d->n_blocks) * 4, t->stream));
   k_validate_calls<<<grid_for(d->n_calls), NTHREADS, 0, t->stream>>>(v, err);
   k_validate_aeg<<<grid_for(d->n_aeg_nodes), NTHREADS, 0, t->stream>>>(v, err);
@@ -232,7 +232,7 @@ saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d) {
   count_launch(3);
   SAGA_CK_LAUNCH();
   VErr h{};
-  SAGA_CK(cudaMemcpyAsync(&h, err, sizeof(VErr), cudaMemcpyDeviceToHost, t->stream));
+  SAGA_CK(d2h(&h, err, sizeof(VErr), t->stream));
   SAGA_CK(cudaStreamSynchronize(t->stream));
   if (h.flags) {
     set_error("saga_load_trace: invalid trace: %s (first offending index %u)", rule_name(h.flags), h.first);

@@ -293,9 +293,9 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     prof_end(SAGA_PROF_EPOCH, s);
     count_launch();
     uint32_t hw[2] = {0, 0}, hn = 0;
-    SAGA_CK(cudaMemcpyAsync(hw, sw, 8, cudaMemcpyDeviceToHost, s));
-    SAGA_CK(cudaMemcpyAsync(&hn, nl, 4, cudaMemcpyDeviceToHost, s));
     SAGA_CK_LAUNCH();
+    SAGA_CK(d2h(hw, sw, 8, s));
+    SAGA_CK(d2h(&hn, nl, 4, s));
     SAGA_CK(cudaStreamSynchronize(s));
     nd.w_lo = hw[0];
     nd.w_hi = hw[1];
@@ -317,7 +317,7 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     count_launch(2);
     SAGA_CK(scan_u32(t, flag, pos, nc));
     uint32_t nu = 0;
-    SAGA_CK(cudaMemcpyAsync(&nu, pos + nc, 4, cudaMemcpyDeviceToHost, s));
+    SAGA_CK(d2h(&nu, pos + nc, 4, s));
     SAGA_CK(cudaStreamSynchronize(s));
     nd.n_upd = nu;
     nd.upd_c = dalloc<uint32_t>(t, nu);

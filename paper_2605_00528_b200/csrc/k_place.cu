@@ -520,8 +520,8 @@ saga_status run_placement(saga_trace* t) {
   SAGA_CK_LAUNCH();
   uint32_t hn[4];
   unsigned long long hs[2];
-  SAGA_CK(cudaMemcpyAsync(hn, out_n, 16, cudaMemcpyDeviceToHost, t->stream));
-  SAGA_CK(cudaMemcpyAsync(hs, out_stats, 16, cudaMemcpyDeviceToHost, t->stream));
+  SAGA_CK(d2h(hn, out_n, 16, t->stream));
+  SAGA_CK(d2h(hs, out_stats, 16, t->stream));
   SAGA_CK(cudaStreamSynchronize(t->stream));
   if (hn[2]) {
     set_error("saga_load_trace: placement limit exceeded (%s); queue capacity %u calls per node",

@@ -1188,8 +1188,8 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   }
   SAGA_CK(scan_u32(t, head, hpos, N));
   uint32_t hv[2] = {0, 0};
-  SAGA_CK(cudaMemcpyAsync(&hv[0], hpos + N, 4, cudaMemcpyDeviceToHost, s));
-  SAGA_CK(cudaMemcpyAsync(&hv[1], s2lo + NS, 4, cudaMemcpyDeviceToHost, s));
+  SAGA_CK(d2h(&hv[0], hpos + N, 4, s));
+  SAGA_CK(d2h(&hv[1], s2lo + NS, 4, s));
   SAGA_CK(cudaStreamSynchronize(s));
   const uint32_t nu = hv[0];
   nd.n_units = nu;
@@ -1351,10 +1351,10 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
     set_error("out of device memory (replay scratch %llu bytes)", (unsigned long long)(a.cta_bytes * grid));
     return SAGA_ERR_OOM;
   }
-  SAGA_CK(cudaMemcpyAsync(d_nodes, hn.data(), sizeof(NodeArr) * t->n_nodes, cudaMemcpyHostToDevice, s));
-  SAGA_CK(cudaMemcpyAsync(d_caps, caps, 4 * n_caps, cudaMemcpyHostToDevice, s));
-  SAGA_CK(cudaMemcpyAsync(d_list, nodes, 4 * n_owned, cudaMemcpyHostToDevice, s));
-  SAGA_CK(cudaMemcpyAsync(d_items, items.data(), 4 * n_items, cudaMemcpyHostToDevice, s));
+  SAGA_CK(h2d(d_nodes, hn.data(), sizeof(NodeArr) * t->n_nodes, s));
+  SAGA_CK(h2d(d_caps, caps, 4 * n_caps, s));
+  SAGA_CK(h2d(d_list, nodes, 4 * n_owned, s));
+  SAGA_CK(h2d(d_items, items.data(), 4 * n_items, s));
   SAGA_CK(cudaMemsetAsync(work, 0, 32, s));
   a.v = v;
   a.nodes = d_nodes; a.caps = d_caps; a.items = d_items; a.n_items = n_items; a.node_list = d_list;
@@ -1371,10 +1371,10 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   count_launch();
   SAGA_CK_LAUNCH();
   uint32_t hw[8] = {0};
-  SAGA_CK(cudaMemcpyAsync(hw, work, 32, cudaMemcpyDeviceToHost, s));
+  SAGA_CK(d2h(hw, work, 32, s));
   const uint32_t& herr = hw[1];
   std::vector<unsigned long long> cyc(trace ? 9ull * n_items : 0);
-  if (trace) SAGA_CK(cudaMemcpyAsync(cyc.data(), d_cyc, 8ull * 9 * n_items, cudaMemcpyDeviceToHost, s));
+  if (trace) SAGA_CK(d2h(cyc.data(), d_cyc, 8ull * 9 * n_items, s));
   ws_free(d_nodes, s); ws_free(d_caps, s); ws_free(d_list, s); ws_free(d_items, s);
   ws_free(scratch, s);
   ws_free(work, s);

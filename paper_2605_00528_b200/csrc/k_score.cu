@@ -333,7 +333,7 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
   for (uint32_t w = 0; w < t->n_nodes; ++w) { hn[w].lown = t->nodes[w].lown; hn[w].n_local = t->nodes[w].n_local; }
   ScoreNode* dn = nullptr;
   SAGA_CK(ws_malloc((void**)&dn, sizeof(ScoreNode) * t->n_nodes, s));
-  SAGA_CK(cudaMemcpyAsync(dn, hn.data(), sizeof(ScoreNode) * t->n_nodes, cudaMemcpyHostToDevice, s));
+  SAGA_CK(h2d(dn, hn.data(), sizeof(ScoreNode) * t->n_nodes, s));
   ScoreArgs a{};
   a.v = t->v; a.nodes = dn; a.b = *b;
   a.alpha = cfg->alpha; a.beta = cfg->beta; a.gamma = cfg->gamma;
@@ -354,7 +354,7 @@ saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint3
   if (n_seg == 0) return SAGA_OK;
   // scratch: per CTA the largest power of two >= the largest segment (sizes read back once)
   std::vector<uint64_t> off(size_t(n_seg) + 1);
-  SAGA_CK(cudaMemcpyAsync(off.data(), seg_off, 8 * (size_t(n_seg) + 1), cudaMemcpyDeviceToHost, s));
+  SAGA_CK(d2h(off.data(), seg_off, 8 * (size_t(n_seg) + 1), s));
   SAGA_CK(cudaStreamSynchronize(s));
   uint64_t mx = 1;
   for (uint32_t i = 0; i < n_seg; ++i) mx = std::max<uint64_t>(mx, off[i + 1] - off[i]);

@@ -114,6 +114,50 @@ void ws_free(void* p, cudaStream_t s) {
     if (b.p == p) { b.used = false; b.s = s; return; }
 }
 
+// pinned bounce buffers for d2h / h2d, one per concurrent caller
+namespace bounce_detail {
+constexpr size_t kBounce = 64 * 1024;
+std::mutex g_mu;
+std::vector<void*> g_free;
+void* take() {
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    if (!g_free.empty()) { void* p = g_free.back(); g_free.pop_back(); return p; }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, kBounce, cudaHostAllocPortable) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  return p;
+}
+void give(void* p) {
+  std::lock_guard<std::mutex> g(g_mu);
+  g_free.push_back(p);
+}
+}  // namespace bounce_detail
+
+cudaError_t d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
+  using namespace bounce_detail;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess || n == 0) return e;
+  void* b = n <= kBounce ? take() : nullptr;
+  if ((e = cudaMemcpyAsync(b ? b : dst, src, n, cudaMemcpyDeviceToHost, s)) == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (b) {
+    if (e == cudaSuccess) memcpy(dst, b, n);
+    give(b);
+  }
+  return e;
+}
+
+cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
+  using namespace bounce_detail;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess || n == 0) return e;
+  void* b = n <= kBounce ? take() : nullptr;
+  if (b) memcpy(b, src, n);
+  if ((e = cudaMemcpyAsync(dst, b ? b : src, n, cudaMemcpyHostToDevice, s)) == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (b) give(b);
+  return e;
+}
+
 static void mempool_setup(int device) {
   static std::mutex mu;
   static uint64_t done_mask = 0;
@@ -187,8 +231,22 @@ void saga_free_trace(saga_trace* t) {
   delete t;
 }
 
+// A3 of a node on first use when the load deferred it (SAGA_LOAD_DEFER_EXPAND)
+static saga_status ensure_expanded(saga_trace* t, uint32_t w) {
+  NodeDev& nd = t->nodes[w];
+  if (nd.expanded) return SAGA_OK;
+  const saga_status st = run_expand(t, w);
+  if (st == SAGA_OK) nd.expanded = true;
+  return st;
+}
+
 saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask, int device,
                             saga_stream_t stream, saga_trace** out) {
+  return saga_load_trace_ex(desc, cfg, owned_node_mask, device, stream, 0u, out);
+}
+
+saga_status saga_load_trace_ex(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask,
+                               int device, saga_stream_t stream, uint32_t flags, saga_trace** out) {
   g_err.clear();
   if (!desc || !cfg || !out) { set_error("saga_load_trace: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   *out = nullptr;
@@ -221,7 +279,8 @@ saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* c
   for (uint32_t w = 0; w < desc->n_nodes; ++w) {
     if (!((t->owned_mask >> w) & 1u)) continue;
     t->nodes[w].owned = true;
-    st = run_expand(t, w);
+    if (flags & SAGA_LOAD_DEFER_EXPAND) continue;
+    st = ensure_expanded(t, w);
     if (st != SAGA_OK) { saga_free_trace(t); return st; }
   }
   cudaError_t e = cudaStreamSynchronize(t->stream);
@@ -237,6 +296,9 @@ saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* c
 saga_status saga_trace_info(const saga_trace* t, uint32_t node, uint64_t* n_access, uint32_t* n_local_blocks) {
   CHECK_HANDLE(t);
   if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_trace_info: node %u not owned", node); return SAGA_ERR_STATE; }
+  saga_trace* tm = const_cast<saga_trace*>(t);  // lazy A3 only; the trace is not otherwise modified
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(tm, ensure_expanded(tm, node));
   const NodeDev& nd = t->nodes[node];
   if (n_access) *n_access = nd.N;
   if (n_local_blocks) *n_local_blocks = nd.nu_done ? nd.n_local : UINT32_MAX;
@@ -246,10 +308,10 @@ saga_status saga_trace_info(const saga_trace* t, uint32_t node, uint64_t* n_acce
 saga_status saga_placement(const saga_trace* t, uint8_t* node_host, uint32_t* mig_host, uint64_t mig_cap, int64_t* stats) {
   CHECK_HANDLE(t);
   SAGA_CK(cudaSetDevice(t->device));
-  if (node_host) SAGA_CK(cudaMemcpyAsync(node_host, t->node_of, t->n_calls, cudaMemcpyDeviceToHost, t->stream));
+  if (node_host) SAGA_CK(d2h(node_host, t->node_of, t->n_calls, t->stream));
   if (mig_host && mig_cap) {
     uint64_t n = std::min<uint64_t>(mig_cap, t->n_mig);
-    if (n) SAGA_CK(cudaMemcpyAsync(mig_host, t->migs, n * sizeof(Mig), cudaMemcpyDeviceToHost, t->stream));
+    if (n) SAGA_CK(d2h(mig_host, t->migs, n * sizeof(Mig), t->stream));
   }
   SAGA_CK(cudaStreamSynchronize(t->stream));
   if (stats) { stats[0] = t->n_steals; stats[1] = t->n_reroutes; stats[2] = t->n_mig; }
@@ -260,6 +322,9 @@ saga_status saga_node_stream_sizes(const saga_trace* t, uint32_t node, uint64_t*
                                    uint32_t* n_groups, uint32_t* n_inv) {
   CHECK_HANDLE(t);
   if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("node %u not owned", node); return SAGA_ERR_STATE; }
+  saga_trace* tm = const_cast<saga_trace*>(t);  // lazy A3 only
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(tm, ensure_expanded(tm, node));
   const NodeDev& nd = t->nodes[node];
   if (n_access) *n_access = nd.N;
   if (n_events) *n_events = nd.J;
@@ -317,6 +382,7 @@ saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_us
   if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_belady_next_use: node %u not owned", node); return SAGA_ERR_STATE; }
   SAGA_CK(cudaSetDevice(t->device));
   GUARD(t, join((cudaStream_t)stream, t->stream));
+  GUARD(t, ensure_expanded(t, node));
   GUARD(t, run_next_use(t, node, next_use_dev, local_id_dev, t->stream));
   GUARD(t, join(t->stream, (cudaStream_t)stream));
   return SAGA_OK;

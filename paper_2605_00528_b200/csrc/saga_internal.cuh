@@ -31,6 +31,14 @@ void set_error(const char* fmt, ...);
 cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s);
 void ws_free(void* p, cudaStream_t s);
 
+// Small host<->device copies of the host-side control flow (sizes, flags, launch tables).  Both
+// wait for the stream first and move the bytes through a pinned bounce buffer, then wait again:
+// a copy from or to pageable memory blocks inside the driver's staging path until the stream
+// reaches it, which stalls every other host thread's pageable copy behind a long kernel (two
+// steps in flight on two streams would serialise).  Synchronous: the bytes are in place on return.
+cudaError_t d2h(void* dst, const void* src, size_t n, cudaStream_t s);
+cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t s);
+
 // device-time profile (saga_profile_enable / saga_profile_read)
 void prof_begin(int cat, cudaStream_t s);
 void prof_end(int cat, cudaStream_t s);
@@ -87,6 +95,7 @@ struct TraceView {
 
 struct NodeDev {
   bool owned = false;
+  bool expanded = false;       // A3 done (deferred with SAGA_LOAD_DEFER_EXPAND)
   uint64_t N = 0;          // accesses
   uint32_t J = 0;          // events incl. the trailing sentinel
   uint32_t G = 0;          // record groups

@@ -70,6 +70,7 @@ def _load():
         "saga_last_error": (C.c_char_p, []),
         "saga_kernel_launches": (u64, []),
         "saga_load_trace": (i32, [C.POINTER(TraceDescC), C.POINTER(PlaceCfgC), u32, i32, vp, C.POINTER(vp)]),
+        "saga_load_trace_ex": (i32, [C.POINTER(TraceDescC), C.POINTER(PlaceCfgC), u32, i32, vp, u32, C.POINTER(vp)]),
         "saga_trace_info": (i32, [vp, u32, C.POINTER(u64), C.POINTER(u32)]),
         "saga_placement": (i32, [vp, vp, vp, u64, vp]),
         "saga_node_stream_sizes": (i32, [vp, u32, C.POINTER(u64), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
@@ -147,7 +148,8 @@ class HostDesc:
 class Trace:
     """A loaded trace handle (saga_load_trace).  All methods are stream-ordered on `stream`."""
 
-    def __init__(self, desc, place_cfg: dict, owned_mask: int = 0, device: int = 0, stream=None, host=None):
+    def __init__(self, desc, place_cfg: dict, owned_mask: int = 0, device: int = 0, stream=None, host=None,
+                 defer_expand: bool = False):
         import torch
         self.desc = desc
         self.device = device
@@ -155,8 +157,8 @@ class Trace:
         self._host = host if host is not None else HostDesc(desc)
         self._pc = place_cfg_c(place_cfg)
         h = C.c_void_p()
-        _check(lib.saga_load_trace(C.byref(self._host.c), C.byref(self._pc), owned_mask, device,
-                                   _stream_ptr(self.stream), C.byref(h)))
+        _check(lib.saga_load_trace_ex(C.byref(self._host.c), C.byref(self._pc), owned_mask, device,
+                                      _stream_ptr(self.stream), 1 if defer_expand else 0, C.byref(h)))
         self.h = h
 
     def free(self):
