@@ -37,7 +37,7 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "trace accesses/sec (AEG score+evict+replay, Bélády); HBM GB/s vs B200 peak"
 UNIT = "access-replays/s"
-PROF_NAMES = ["load", "place", "expand", "sort", "segscan", "epoch_stats", "replay", "score", "select"]
+PROF_NAMES = ["load", "place", "expand", "sort", "segscan", "epoch_stats", "replay", "score", "select", "pattern"]
 WORKLOADS = {
     "C1": "tiny trace: 8 sessions x 10 calls, 1 node, 64 KV blocks",
     "C2": "SWE-bench-shaped: 2000 sessions, 10-100 calls/task, 16-token blocks, 8 nodes, 8+1 caps",
@@ -437,8 +437,8 @@ def main():
     barrier()
     launches = saga.kernel_launches() - l0
     import ctypes as C
-    pm = (C.c_double * 9)()
-    pn = (C.c_uint64 * 9)()
+    pm = (C.c_double * len(PROF_NAMES))()
+    pn = (C.c_uint64 * len(PROF_NAMES))()
     saga.lib.saga_profile_read(pm, pn)
     saga.lib.saga_profile_enable(0)
     clocks = sampler.stop()

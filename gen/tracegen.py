@@ -48,6 +48,8 @@ TOOLS = {
     "Database": (120.0, 890.0),
 }
 TOOL_ORDER = ["FileOps", "CodeExec", "WebApi", "Database"]
+# observable tool-type labels of calls (F3 pattern inference): Table 1's classes + run_test
+TOOL_LABELS = TOOL_ORDER + ["RunTest"]
 
 
 def tool_params(name: str):
@@ -86,6 +88,9 @@ class TraceDesc:
     type_shared_len: np.ndarray
     block_tokens: int = BLOCK_TOKENS
     seed: int = 0
+    # generator metadata, not part of saga_trace_desc: tool type phi(v) of each AEG node, the label
+    # a request stream exposes (F3); index into TOOL_LABELS
+    node_tool: Optional[np.ndarray] = None
 
     @property
     def n_calls(self):
@@ -148,6 +153,70 @@ def default_replay_cfg(policy_mask: int = 3) -> dict:
 # helpers
 # ----------------------------------------------------------------------------------------------
 
+def pattern_labels(d: TraceDesc) -> np.ndarray:
+    """Observed label of each call (F3): the tool type phi(v) of its AEG node, uint32."""
+    if d.node_tool is None:
+        return np.zeros(d.n_calls, np.uint32)
+    return np.asarray(d.node_tool, np.uint32)[np.asarray(d.call_aeg_node, np.int64)]
+
+
+def pattern_roles(d: TraceDesc, held_out_frac: float = 0.5, seed: int = 12345) -> np.ndarray:
+    """Session roles for F3 (uint8): a seeded random held_out_frac of the sessions is held out (2),
+    the others train (1)."""
+    rng = np.random.default_rng(seed)
+    return np.where(rng.random(d.n_sessions) < held_out_frac, 2, 1).astype(np.uint8)
+
+
+def make_label_markov(seed: int, n_sessions: int, trans: np.ndarray, start: int = 0, n_types: int = 1,
+                      max_len: int = 200) -> TraceDesc:
+    """Sessions whose label sequences follow a first-order Markov chain over labels (F3 pins):
+    trans[x][y] for y < L is P(x -> y), trans[x][L] the probability that the task ends.  AEG node
+    of a call = its label (node_tool = identity); one private block per call, one node; session
+    s has type s % n_types; calls spaced so that sessions interleave."""
+    rng = np.random.default_rng(seed)
+    trans = np.asarray(trans, np.float64)
+    L = trans.shape[0]
+    b = _AEGBuilder()
+    for x in range(L):
+        b.add_node(1_000_000, 0, False, tool=x)
+    for x in range(L):
+        for y in range(L):
+            if trans[x, y] > 0:
+                b.add_edge(x, y, float(trans[x, y]))
+    aeg = b.finish()
+    t, s, v, last = [], [], [], []
+    for ss in range(n_sessions):
+        x = start
+        for j in range(max_len):
+            t.append(1 + ss * 7_919 + j * 1_000_003); s.append(ss); v.append(x)
+            y = int(rng.choice(L + 1, p=trans[x] / trans[x].sum()))
+            if y == L or j == max_len - 1:
+                last.append(1)
+                break
+            last.append(0)
+            x = y
+    order = np.lexsort((np.array(s), np.array(t)))
+    n = len(t)
+    cnt = np.bincount(np.array(s), minlength=n_sessions)
+    slo = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.uint32)
+    # call k of session s touches private block slo[s] + (its index within the session)
+    s_arr = np.array(s)[order]
+    idx = np.zeros(n, np.int64)
+    seen = np.zeros(n_sessions, np.int64)
+    for i, ss in enumerate(s_arr):
+        idx[i] = seen[ss]; seen[ss] += 1
+    return TraceDesc(
+        name="label_markov", n_nodes=1, n_blocks=int(n) + 1, seed=seed,
+        call_t_us=np.array(t, np.int64)[order], call_session=s_arr.astype(np.uint32),
+        call_aeg_node=np.array(v, np.uint32)[order], call_prompt_tokens=np.full(n, 16, np.uint32),
+        call_output_tokens=np.full(n, 1, np.uint32), call_new_tokens=np.full(n, 16, np.uint32),
+        call_is_last=np.array(last, np.uint8)[order], call_range_off=np.arange(n + 1, dtype=np.uint32),
+        range_block_lo=(slo[s_arr] + idx).astype(np.uint32), range_len=np.ones(n, np.uint32),
+        session_type=(np.arange(n_sessions) % n_types).astype(np.uint16),
+        session_block_lo=slo, session_block_len=cnt.astype(np.uint32),
+        type_shared_lo=np.zeros(n_types, np.uint32), type_shared_len=np.zeros(n_types, np.uint32), **aeg)
+
+
 def _seg(n_steps: np.ndarray):
     """flat (session, step) index arrays for sessions with n_steps[s] steps."""
     n_steps = n_steps.astype(np.int64)
@@ -201,12 +270,14 @@ class _AEGBuilder:
         self.ttl: List[int] = []
         self.obs: List[int] = []
         self.term: List[int] = []
+        self.tool: List[int] = []
 
-    def add_node(self, ttl_us, obs, terminal):
+    def add_node(self, ttl_us, obs, terminal, tool=0):
         self.edges.append([])
         self.ttl.append(int(ttl_us))
         self.obs.append(int(obs))
         self.term.append(int(terminal))
+        self.tool.append(int(tool))
         return len(self.edges) - 1
 
     def add_edge(self, u, v, p, q16=65536):
@@ -222,7 +293,7 @@ class _AEGBuilder:
         return dict(aeg_edge_off=np.array(off, np.uint32), edge_dst=np.array(dst, np.uint32),
                     edge_p=np.array(p, np.float32), edge_shared_q16=np.array(q, np.uint32),
                     node_ttl_base_us=np.array(self.ttl, np.int64), node_obs_tokens=np.array(self.obs, np.uint32),
-                    node_terminal=np.array(self.term, np.uint8))
+                    node_terminal=np.array(self.term, np.uint8), node_tool=np.array(self.tool, np.uint32))
 
 
 # ----------------------------------------------------------------------------------------------
@@ -236,10 +307,12 @@ def _swe_aeg(b: _AEGBuilder, max_steps=100, p_geo=1 / 29.24):
            "edit_code": _p95_us(*tool_params("CodeExec")),
            "run_test": _p95_us(math.log(2400.0), 1.0)}
     obs = {"read_file": 1250, "edit_code": 175, "run_test": 850}
+    label = {"read_file": TOOL_LABELS.index("FileOps"), "edit_code": TOOL_LABELS.index("CodeExec"),
+             "run_test": TOOL_LABELS.index("RunTest")}
     base = len(b.edges)
     for i in range(max_steps):
         k = cyc[i % 3]
-        b.add_node(ttl[k], obs[k], i == max_steps - 1)
+        b.add_node(ttl[k], obs[k], i == max_steps - 1, tool=label[k])
     for i in range(max_steps - 1):
         b.add_edge(base + i, base + i + 1, 1.0 if i < 9 else 1.0 - p_geo)
     return base
@@ -282,7 +355,7 @@ def _webarena_aeg(b: _AEGBuilder, max_steps=60, p_geo=1 / 18, shares=(0.45, 0.55
     base = len(b.edges)
     for i in range(max_steps):
         for a in range(3):
-            b.add_node(ttl[a], 6000, i == max_steps - 1)
+            b.add_node(ttl[a], 6000, i == max_steps - 1, tool=TOOL_LABELS.index(tools[a][0]))
     probs = (0.5, 0.3, 0.2)
     for i in range(max_steps - 1):
         for a in range(3):
@@ -326,7 +399,7 @@ def _chain_aeg(b: _AEGBuilder, n_steps, rng, obs_tokens):
     base = len(b.edges)
     tools = rng.integers(0, 4, size=n_steps)
     for i in range(n_steps):
-        b.add_node(_p95_us(*tool_params(TOOL_ORDER[tools[i]])), obs_tokens, i == n_steps - 1)
+        b.add_node(_p95_us(*tool_params(TOOL_ORDER[tools[i]])), obs_tokens, i == n_steps - 1, tool=int(tools[i]))
     for i in range(n_steps - 1):
         b.add_edge(base + i, base + i + 1, 1.0)
     return base, tools
@@ -463,7 +536,7 @@ def make_c1(limit_case: bool = False) -> TraceDesc:
     b = _AEGBuilder()
     for j in range(10):
         ttl = 10_000_000 if limit_case else (320_000 if j % 2 == 0 else 2_400_000)
-        b.add_node(ttl, 160 if j % 2 == 0 else 64, j == 9)
+        b.add_node(ttl, 160 if j % 2 == 0 else 64, j == 9, tool=j % 2)
     for j in range(9):
         b.add_edge(j, j + 1, 1.0)
     aeg = b.finish()
@@ -667,7 +740,8 @@ def make_random_small(seed: int, n_sessions: int = 5, n_nodes: int = 2, max_call
     b = _AEGBuilder()
     n_aeg = 6
     for i in range(n_aeg):
-        b.add_node(int(rng.choice([50_000, 150_000, 400_000, 2_000_000])), int(rng.integers(0, 400)), i == n_aeg - 1)
+        b.add_node(int(rng.choice([50_000, 150_000, 400_000, 2_000_000])), int(rng.integers(0, 400)), i == n_aeg - 1,
+                   tool=i % len(TOOL_LABELS))
     for i in range(n_aeg - 1):
         ds = sorted(set(int(x) for x in rng.integers(i + 1, n_aeg, size=int(rng.integers(1, 3)))))
         ps = rng.dirichlet(np.ones(len(ds) + 1))[:len(ds)]

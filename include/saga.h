@@ -15,6 +15,7 @@
  *   saga_evict_select    A6 capacity-bounded top-k (evict the largest keys)
  *   saga_replay          A7 epoch-synchronous replay of hits/misses per (policy, node, capacity)
  *   saga_allreduce_counters  A8 counter reduction over NCCL (NVLink / NVSwitch)
+ *   saga_pattern_infer   F3 pattern-based AEG inference from observed label sequences
  *
  * Conventions for every function:
  *   - Return a saga_status; nothing aborts, exits or throws across the ABI.  The message of the
@@ -247,6 +248,36 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream);
 
+/* F3.  Pattern-based AEG inference, observability tier (b) of §3.3 (P:645:
+ * "extracting tool-type patterns, computing transition probabilities, and retaining edges
+ * exceeding theta_conf = 0.7"; cold start "until 30 tasks complete") and the next-step accuracy
+ * of tab:pattern ("fraction of correctly predicted next-step node transitions in
+ * held-out traces").  Readings R-pattern in DESIGN.md §3: first-order (bigram) transitions of
+ * the observed label sequence of each session, "exceeding" read as >=, the end of a completed
+ * task is successor y = n_labels.
+ *   call_label_dev  uint32[n_calls] observed label (tool type) of each call, < n_labels <= 64
+ *   session_role_dev uint8[n_sessions]: 0 ignored, 1 training, 2 held-out
+ *   theta_pm        theta_conf in per-mille (700), 1..1000; min_tasks the cold start (30)
+ * Outputs (device, overwritten):
+ *   counts_dev uint64[n_types][n_labels][n_labels+1]: over the calls of training sessions of
+ *              type a, consecutive calls labelled x then y, and y = n_labels for a session's
+ *              final call when it carries call_is_last;
+ *   tasks_dev  uint32[n_types]: completed training sessions of each type;
+ *   pred_dev   uint32[n_types][n_labels]: when tasks[a] >= min_tasks, the successor y with
+ *              1000 * counts[a][x][y] >= theta_pm * sum_y counts[a][x][y] and the largest count
+ *              (smallest y on ties); SAGA_PATTERN_NONE otherwise;
+ *   prob_dev   float[n_types][n_labels][n_labels+1] (nullable): (float)counts / (float)total of
+ *              every retained edge (fp32 round-to-nearest division), 0 elsewhere;
+ *   eval_dev   uint64[n_types][4] (nullable): over held-out sessions, {transitions (same
+ *              definition as counts), predicted (pred != NONE), correct (pred == y), 0}.
+ * Integer outputs are exact.  SAGA_ERR_INVALID_ARG for a label >= n_labels (checked on the
+ * device; syncs once at the end) or arguments out of range. */
+enum { SAGA_PATTERN_NONE = 0xFFFFFFFFu };
+saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_dev, uint32_t n_labels,
+                               const uint8_t* session_role_dev, uint32_t theta_pm, uint32_t min_tasks,
+                               uint64_t* counts_dev, uint32_t* tasks_dev, uint32_t* pred_dev, float* prob_dev,
+                               uint64_t* eval_dev, saga_stream_t stream);
+
 /* A8.  NCCL communicator from a 128-byte ncclUniqueId exchanged by the caller (e.g. over
  * torch.distributed).  The library dlopen()s libnccl.so.2 (the process's copy if loaded). */
 saga_status saga_comm_unique_id(void* id128);
@@ -271,7 +302,8 @@ enum {
   SAGA_PROF_REPLAY = 6,    /* A5-A7 replay kernel                                             */
   SAGA_PROF_SCORE = 7,     /* A5 bulk score                                                   */
   SAGA_PROF_SELECT = 8,    /* A6 bulk select                                                  */
-  SAGA_PROF_NCAT = 9
+  SAGA_PROF_PATTERN = 9,   /* F3 pattern inference (count + predict + evaluate)               */
+  SAGA_PROF_NCAT = 10
 };
 void saga_profile_enable(int on);
 void saga_profile_read(double* ms_out, uint64_t* n_out);

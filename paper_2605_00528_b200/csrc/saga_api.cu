@@ -428,6 +428,27 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
   return run_select(key_dev, seg_off_dev, k_dev, n_seg, out_off_dev, victim_idx_dev, (cudaStream_t)stream);
 }
 
+saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_dev, uint32_t n_labels,
+                               const uint8_t* session_role_dev, uint32_t theta_pm, uint32_t min_tasks,
+                               uint64_t* counts_dev, uint32_t* tasks_dev, uint32_t* pred_dev, float* prob_dev,
+                               uint64_t* eval_dev, saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if ((t->n_calls && !call_label_dev) || (t->n_sessions && !session_role_dev) || !counts_dev || !tasks_dev || !pred_dev) {
+    set_error("saga_pattern_infer: NULL argument");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  if (n_labels == 0 || n_labels > 64 || theta_pm == 0 || theta_pm > 1000) {
+    set_error("saga_pattern_infer: need 1 <= n_labels <= 64 and 1 <= theta_pm <= 1000");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  SAGA_CK(cudaSetDevice(t->device));
+  const cudaStream_t s = stream ? (cudaStream_t)stream : t->stream;
+  GUARD(const_cast<saga_trace*>(t), join(t->stream, s));
+  GUARD(const_cast<saga_trace*>(t), run_pattern(t, call_label_dev, n_labels, session_role_dev, theta_pm, min_tasks,
+                                                counts_dev, tasks_dev, pred_dev, prob_dev, eval_dev, s));
+  return SAGA_OK;
+}
+
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream) {
   CHECK_HANDLE(t);

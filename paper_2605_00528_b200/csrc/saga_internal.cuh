@@ -273,6 +273,9 @@ saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint3
                        const uint64_t* out_off, uint32_t* victim, cudaStream_t s);
 saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                        const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s);
+saga_status run_pattern(const saga_trace* t, const uint32_t* label, uint32_t n_labels, const uint8_t* role,
+                        uint32_t theta_pm, uint32_t min_tasks, uint64_t* counts, uint32_t* tasks, uint32_t* pred,
+                        float* prob, uint64_t* eval, cudaStream_t s);
 
 // radix sort of (key u32, value = position) pairs: sorted keys and values into *_out
 cudaError_t onesweep_sort_pairs(saga_trace* t, const uint32_t* keys_in, uint64_t n, uint32_t key_bits,

@@ -80,6 +80,7 @@ def _load():
         "saga_aeg_score": (i32, [vp, C.POINTER(ScoreBatchC), C.POINTER(ReplayCfgC), vp, vp, vp]),
         "saga_evict_select": (i32, [vp, vp, vp, u32, vp, vp, vp]),
         "saga_replay": (i32, [vp, C.POINTER(ReplayCfgC), vp, u32, vp, u32, vp, vp]),
+        "saga_pattern_infer": (i32, [vp, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp, vp]),
         "saga_comm_unique_id": (i32, [vp]),
         "saga_comm_init": (i32, [vp, i32, i32, i32, C.POINTER(vp)]),
         "saga_allreduce_counters": (i32, [vp, vp, C.c_size_t, i32, vp]),
@@ -222,6 +223,28 @@ class Trace:
         cfg = replay_cfg_c(rcfg)
         _check(lib.saga_replay(self.h, C.byref(cfg), caps.ctypes.data, caps.size, nodes.ctypes.data, nodes.size,
                                counters.data_ptr(), _stream_ptr(self.stream)))
+
+    def pattern_infer(self, label, n_labels: int, role, theta_pm: int = 700, min_tasks: int = 30,
+                      want_prob: bool = True, want_eval: bool = True):
+        """F3 (saga_pattern_infer): label uint32/int32 cuda tensor [n_calls], role uint8 cuda tensor
+        [n_sessions] (0 ignored, 1 training, 2 held-out).  Returns a dict of cuda tensors: counts
+        int64 [T, L, L+1], tasks int32 [T], pred int32 [T, L] (-1 = none), prob float32
+        [T, L, L+1], eval int64 [T, 4] (transitions, predicted, correct, 0)."""
+        import torch
+        dev = label.device
+        T, L = self.desc.n_types, int(n_labels)
+        out = dict(counts=torch.empty((T, L, L + 1), dtype=torch.int64, device=dev),
+                   tasks=torch.empty(T, dtype=torch.int32, device=dev),
+                   pred=torch.empty((T, L), dtype=torch.int32, device=dev))
+        if want_prob:
+            out["prob"] = torch.empty((T, L, L + 1), dtype=torch.float32, device=dev)
+        if want_eval:
+            out["eval"] = torch.empty((T, 4), dtype=torch.int64, device=dev)
+        ptr = lambda k: out[k].data_ptr() if k in out else None
+        _check(lib.saga_pattern_infer(self.h, label.data_ptr(), L, role.data_ptr(), int(theta_pm), int(min_tasks),
+                                      ptr("counts"), ptr("tasks"), ptr("pred"), ptr("prob"), ptr("eval"),
+                                      _stream_ptr(self.stream)))
+        return out
 
     def aeg_score(self, batch: dict, rcfg: dict, key_out, score_out=None, policy=POLICY_AEG):
         """batch: dict of int/uint torch tensors seg_node, seg_epoch, seg_occ, seg_cap, seg_act (int32),

@@ -17,14 +17,14 @@ import torch  # noqa: E402
 from gen import make, place_cfg_for  # noqa: E402
 from paper_2605_00528_b200 import saga  # noqa: E402
 
-PROF = ["load", "place", "expand", "sort", "segscan", "epoch_stats", "replay", "score", "select"]
+PROF = ["load", "place", "expand", "sort", "segscan", "epoch_stats", "replay", "score", "select", "pattern"]
 
 
 def prof():
-    pm = (C.c_double * 9)()
-    pn = (C.c_uint64 * 9)()
+    pm = (C.c_double * len(PROF))()
+    pn = (C.c_uint64 * len(PROF))()
     saga.lib.saga_profile_read(pm, pn)
-    return {PROF[i]: round(pm[i], 2) for i in range(9) if pn[i]}
+    return {PROF[i]: round(pm[i], 2) for i in range(len(PROF)) if pn[i]}
 
 
 def main():
