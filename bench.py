@@ -184,6 +184,40 @@ def bulk_score_select(t, desc, stream, dev, reps=5, n_seg=1024, seg_len=32768, k
     return out
 
 
+def f3_pattern(stream, dev, reps=5, config="C5"):
+    """SURVEY §8(f) F3 on the largest config (6.4 M calls, inputs >> L2): saga_pattern_infer with
+    the generator's tool labels, half the sessions held out.  Algorithmic bytes per call position
+    and pass (DESIGN.md §6 F3): sc_call 4 + call_sess 4 + role 1 + label 4 + sc_off 4 + next label 4
+    + call_is_last 1 = 22 B; two passes (count, evaluate) -> 44 B per call."""
+    import numpy as np
+    import torch
+    from gen import TOOL_LABELS, make, pattern_labels, pattern_roles, place_cfg_for
+    from paper_2605_00528_b200 import saga
+    d = make(config)
+    t = saga.Trace(d, place_cfg_for(d), stream=stream, defer_expand=True)
+    lab = torch.from_numpy(pattern_labels(d).view(np.int32)).to(dev)
+    role = torch.from_numpy(pattern_roles(d)).to(dev)
+    L = len(TOOL_LABELS)
+    with torch.cuda.stream(stream):
+        out = t.pattern_infer(lab, L, role)
+        stream.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            out = t.pattern_infer(lab, L, role)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ev = out["eval"].cpu().numpy()
+    t.free()
+    n = d.n_calls
+    return {"config": config, "calls": n, "ms": ms, "calls_per_s": n / (ms / 1e3), "bytes_per_call": 44,
+            "algorithmic_gb_s": n * 44 / (ms / 1e3) / 1e9,
+            "held_out_accuracy": float(ev[:, 2].sum()) / max(1, int(ev[:, 0].sum())),
+            "note": "includes the library's one sync per call (label check readback)"}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (oracle/), as it stands, on a bounded sample of the workload."""
     rank = int(os.environ.get("RANK", "0"))
@@ -500,7 +534,7 @@ def main():
                 "traffic": traffic, "peak_source": peak_kind,
                 "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
 
-    bulk = None
+    bulk = pat = None
     if world == 1 and not args.no_bulk:  # single process: no collective may be issued by one rank
         with torch.cuda.stream(stream):
             t_b, _, _ = pipeline.run_step(desc, pc, rcfg, caps_fn, device=local, stream=stream, host=dd)
@@ -511,6 +545,8 @@ def main():
             for kname, kv in bulk.items():
                 if isinstance(kv, dict):
                     kv["frac"] = kv["algorithmic_gb_s"] / peak
+        pat = f3_pattern(stream, dev)
+        pat["frac"] = pat["algorithmic_gb_s"] / peak
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(desc, pc, caps, os.cpu_count() or 1)
@@ -531,7 +567,7 @@ def main():
                        "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
                                     else ("capacity points" if shard_caps else "cache nodes w mod R"))},
             "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels, "bulk_score_select": bulk,
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels, "bulk_score_select": bulk, "f3_pattern": pat,
             "counters_checksum": int(np.bitwise_xor.reduce(counters_host.reshape(-1).view(np.uint64))),
         }
         print(json.dumps(line), flush=True)

@@ -72,3 +72,33 @@ def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, wo
     if comm is not None and world > 1:
         comm.allreduce(counters, op=0, stream=t.stream)
     return t, caps, counters
+
+
+def inferred_aeg_desc(desc, label, n_labels: int, prob, ttl_us, obs_tokens):
+    """The trace re-annotated with the AEG inferred by saga_pattern_infer (F3: "score with the
+    inferred AEG", tier (b) of P:645).  Node (a, x) = a * n_labels + x stands for "agent type a,
+    tool x"; call c moves to node (type of its session, label[c]); edges are the retained
+    (a, x) -> (a, y), y < n_labels, with P = prob[a, x, y] (the kernel's fp32 frequency) and the
+    linear-chain overlap (whole context shared, eq:overlap P:685); no node is terminal (the
+    residual mass is the end of the task).  ttl_us / obs_tokens [n_labels] are the per-tool TTL
+    base and expected observation length the scheduler keeps per tool (Alg. 1 line 2).
+    Host re-indexing only: every number comes from the kernel or the caller."""
+    import dataclasses
+    prob = np.asarray(prob, np.float32)
+    T, L = prob.shape[0], int(n_labels)
+    off, dst, p = [0], [], []
+    for a in range(T):
+        for x in range(L):
+            for y in range(L):
+                if prob[a, x, y] > 0:
+                    dst.append(a * L + y)
+                    p.append(prob[a, x, y])
+            off.append(len(dst))
+    styp = np.asarray(desc.session_type, np.int64)
+    node = styp[np.asarray(desc.call_session, np.int64)] * L + np.asarray(label, np.int64)
+    return dataclasses.replace(
+        desc, name=desc.name + "+inferred", call_aeg_node=node.astype(np.uint32),
+        aeg_edge_off=np.array(off, np.uint32), edge_dst=np.array(dst, np.uint32), edge_p=np.array(p, np.float32),
+        edge_shared_q16=np.full(len(dst), 65536, np.uint32),
+        node_ttl_base_us=np.tile(np.asarray(ttl_us, np.int64), T), node_obs_tokens=np.tile(np.asarray(obs_tokens, np.uint32), T),
+        node_terminal=np.zeros(T * L, np.uint8), node_tool=np.tile(np.arange(L, dtype=np.uint32), T))

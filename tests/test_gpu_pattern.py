@@ -90,3 +90,22 @@ def test_bad_label_and_args():
     out = t.pattern_infer(lab, 4, torch.zeros_like(ro))  # nothing to count
     assert int(out["counts"].sum()) == 0 and bool((out["pred"] == -1).all())
     t.free()
+
+
+def test_replay_with_inferred_aeg_equals_oracle():
+    """'Score with the inferred AEG': the re-annotated trace loads and replays bit-exactly."""
+    from gen import TOOL_LABELS, sweep_caps
+    from oracle import oracle as O
+    from paper_2605_00528_b200 import pipeline
+    d = make("C2", n_sessions=80, n_nodes=4)
+    pc = place_cfg_for(d)
+    L = len(TOOL_LABELS)
+    label, role = pattern_labels(d), pattern_roles(d)
+    got = _run(d, pc, label, L, role, 700, 10)
+    di = pipeline.inferred_aeg_desc(d, label, L, got["prob"], np.full(L, 2_000_000), np.full(L, 300))
+    t, caps, ctr = pipeline.run_step(di, pc, dict(policy_mask=3), lambda lo, hi: sweep_caps(lo, hi, 4))
+    torch.cuda.synchronize()
+    O.build()
+    ref = O.Oracle(di, pc).replay_many(3, caps)
+    assert np.array_equal(ctr.cpu().numpy(), ref)
+    t.free()
