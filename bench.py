@@ -185,10 +185,10 @@ def bulk_score_select(t, desc, stream, dev, reps=5, n_seg=1024, seg_len=32768, k
 
 
 def f3_pattern(stream, dev, reps=5, config="C5"):
-    """SURVEY §8(f) F3 on the largest config (6.4 M calls, inputs >> L2): saga_pattern_infer with
-    the generator's tool labels, half the sessions held out.  Algorithmic bytes per call position
-    and pass (DESIGN.md §6 F3): sc_call 4 + call_sess 4 + role 1 + label 4 + sc_off 4 + next label 4
-    + call_is_last 1 = 22 B; two passes (count, evaluate) -> 44 B per call."""
+    """SURVEY §8(f) F3 on the largest config (6.4 M calls): saga_pattern_infer with the generator's
+    tool labels, half the sessions held out.  Algorithmic bytes (DESIGN.md §6 F3): every call is
+    read by exactly one of the two passes, sc_call 4 + label 4 = 8 B per call; per session role
+    1 x 2 passes + type 2 + sc_off 4 + call_is_last 1 = 9 B."""
     import numpy as np
     import torch
     from gen import TOOL_LABELS, make, pattern_labels, pattern_roles, place_cfg_for
@@ -198,9 +198,12 @@ def f3_pattern(stream, dev, reps=5, config="C5"):
     lab = torch.from_numpy(pattern_labels(d).view(np.int32)).to(dev)
     role = torch.from_numpy(pattern_roles(d)).to(dev)
     L = len(TOOL_LABELS)
+    import ctypes as C
     with torch.cuda.stream(stream):
         out = t.pattern_infer(lab, L, role)
         stream.synchronize()
+        saga.lib.saga_profile_enable(1)
+        saga.lib.saga_profile_read(None, None)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -209,13 +212,20 @@ def f3_pattern(stream, dev, reps=5, config="C5"):
         e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    pm = (C.c_double * len(PROF_NAMES))()
+    pn = (C.c_uint64 * len(PROF_NAMES))()
+    saga.lib.saga_profile_read(pm, pn)
+    saga.lib.saga_profile_enable(0)
+    k_ms = pm[PROF_NAMES.index("pattern")] / reps  # device time of the three kernels
     ev = out["eval"].cpu().numpy()
     t.free()
     n = d.n_calls
-    return {"config": config, "calls": n, "ms": ms, "calls_per_s": n / (ms / 1e3), "bytes_per_call": 44,
-            "algorithmic_gb_s": n * 44 / (ms / 1e3) / 1e9,
+    nbytes = 8 * n + 9 * d.n_sessions
+    return {"config": config, "calls": n, "ms_call": ms, "ms": k_ms, "calls_per_s": n / (ms / 1e3), "bytes": nbytes,
+            "algorithmic_gb_s": nbytes / (k_ms / 1e3) / 1e9,
             "held_out_accuracy": float(ev[:, 2].sum()) / max(1, int(ev[:, 0].sum())),
-            "note": "includes the library's one sync per call (label check readback)"}
+            "note": "ms / GB/s: device time of the three kernels (CUDA events around them); ms_call: the whole "
+                    "API call incl. memsets and its one sync (label check readback)"}
 
 
 def run_reference(args):

@@ -1,7 +1,8 @@
 // F3: pattern-based AEG inference (saga_pattern_infer; §3.3 tier (b), tab:pattern
 // P:1065-1085; readings R-pattern in DESIGN.md §3).
 //
-// Three launches over the session-ordered call list (sc_off / sc_call, built by A1):
+// Three launches over the session-ordered call list (sc_off / sc_call, built by A1), one warp
+// per session (no per-call session / role gathers; the successor label comes by shuffle):
 //   k_pat_count  each position i of a training session emits one transition x -> y (the next
 //                call's label, or y = L for a completed session's final call) into a segmented
 //                histogram [type][x][y], in shared memory when it fits (warp-aggregated with
@@ -10,8 +11,8 @@
 //   k_pat_pred   one thread per (type, x): total, the retained successors (1000 c >= theta t),
 //                the argmax among them (smallest y on ties), fp32 c / t of retained edges;
 //   k_pat_eval   each position of a held-out session: transitions / predicted / correct per type.
-// HBM-bound gathers: per position sc_call (4 B, coalesced), call_sess, role, label, the next
-// call's label, sc_off (4 B each, gathered), call_is_last (1 B); DESIGN.md §6 F3.
+// Algorithmic bytes per pass (DESIGN.md §6 F3): per session role 1 + type 2 + sc_off 4; per call
+// of the pass's sessions sc_call 4 (coalesced) + label 4 (gathered) + call_is_last 1 at the end.
 #include "saga_internal.cuh"
 
 namespace saga {
@@ -36,15 +37,40 @@ struct PatArgs {
   uint32_t* err;      // [0] flag, [1] first offending call
 };
 
-// successor label of position i (session s), PAT_NONE when the session stops without ending
-__device__ __forceinline__ uint32_t succ_of(const PatArgs& a, uint32_t i, uint32_t c, uint32_t s) {
-  const uint32_t end = a.v.sc_off[s + 1];
-  if (i + 1 < end) return a.label[a.v.sc_call[i + 1]];
-  return a.v.call_last[c] ? a.L : PAT_NONE;
-}
-
 __device__ __forceinline__ void bad_label(const PatArgs& a, uint32_t c) {
   if (atomicOr(&a.err[0], 1u) == 0u) a.err[1] = c;
+}
+
+// One warp per session of the wanted role (warp-uniform loop): lane l holds position i0 + l of
+// the session's call list; the successor label comes from lane l + 1 (lane 31 reads it), or is
+// L ("task ended") at a completed session's final call.  Returns via f(lane's bin or PAT_NONE, y).
+template <class F>
+__device__ __forceinline__ void for_each_transition(const PatArgs& a, uint8_t want, F&& f) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nw = gridDim.x * (PT / 32);
+  for (uint32_t s = (blockIdx.x * PT + threadIdx.x) >> 5; s < a.v.n_sessions; s += nw) {
+    if (a.role[s] != want) continue;
+    const uint32_t b = a.v.sc_off[s], e = a.v.sc_off[s + 1];
+    const uint32_t typ = a.v.styp[s];
+    for (uint32_t i0 = b; i0 < e; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint32_t c = 0, x = PAT_NONE;
+      if (i < e) { c = a.v.sc_call[i]; x = a.label[c]; }
+      uint32_t xn = __shfl_down_sync(0xffffffffu, x, 1);
+      if (lane == 31 && i + 1 < e) xn = a.label[a.v.sc_call[i + 1]];
+      uint32_t x_ok = PAT_NONE, y = PAT_NONE;
+      if (i < e) {
+        if (x >= a.L) {
+          bad_label(a, c);
+        } else {
+          y = i + 1 < e ? xn : (a.v.call_last[c] ? a.L : PAT_NONE);
+          if (y != PAT_NONE && y <= a.L) x_ok = x;  // a bad next label is reported by its own lane
+          else y = PAT_NONE;
+        }
+      }
+      f(typ, x_ok, y);
+    }
+  }
 }
 
 template <bool SMEM>
@@ -55,40 +81,17 @@ __global__ void __launch_bounds__(PT) k_pat_count(PatArgs a) {
     for (uint32_t b = threadIdx.x; b < a.bins; b += PT) hist[b] = 0;
   if (threadIdx.x < 32) s_tasks[threadIdx.x] = 0;
   __syncthreads();
-  const uint32_t n = a.v.n_calls;
   const uint32_t L1 = a.L + 1;
-  // warp-uniform trip count so every lane reaches the warp collectives
-  const uint32_t stride = gridDim.x * PT;
-  for (uint32_t base = blockIdx.x * PT + (threadIdx.x & ~31u); base < n; base += stride) {
-    const uint32_t i = base + (threadIdx.x & 31u);
-    uint32_t bin = PAT_NONE, typ = PAT_NONE;
-    bool ended = false;
-    if (i < n) {
-      const uint32_t c = a.v.sc_call[i];
-      const uint32_t s = a.v.call_sess[c];
-      if (a.role[s] == 1) {
-        const uint32_t x = a.label[c];
-        if (x >= a.L) {
-          bad_label(a, c);
-        } else {
-          const uint32_t y = succ_of(a, i, c, s);
-          if (y != PAT_NONE && y <= a.L) {
-            typ = a.v.styp[s];
-            bin = (typ * a.L + x) * L1 + y;
-            ended = y == a.L;
-          }
-        }
-      }
-    }
+  for_each_transition(a, 1, [&](uint32_t typ, uint32_t x, uint32_t y) {
+    const uint32_t bin = x != PAT_NONE ? (typ * a.L + x) * L1 + y : PAT_NONE;
     if (SMEM) {
       const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-      const int leader = __ffs(peers) - 1;
-      if (bin != PAT_NONE && (int)(threadIdx.x & 31u) == leader) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+      if (bin != PAT_NONE && (int)(threadIdx.x & 31u) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
     } else if (bin != PAT_NONE) {
       atomicAdd(&a.counts[bin], 1ull);
     }
-    if (ended) atomicAdd(&s_tasks[typ], 1u);
-  }
+    if (bin != PAT_NONE && y == a.L) atomicAdd(&s_tasks[typ], 1u);
+  });
   __syncthreads();
   if (SMEM)
     for (uint32_t b = threadIdx.x; b < a.bins; b += PT)
@@ -119,38 +122,21 @@ __global__ void __launch_bounds__(PT) k_pat_eval(PatArgs a) {
   __shared__ unsigned long long s_ev[32 * 3];
   for (uint32_t b = threadIdx.x; b < 32 * 3; b += PT) s_ev[b] = 0;
   __syncthreads();
-  const uint32_t n = a.v.n_calls;
-  const uint32_t stride = gridDim.x * PT;
-  for (uint32_t base = blockIdx.x * PT + (threadIdx.x & ~31u); base < n; base += stride) {
-    const uint32_t i = base + (threadIdx.x & 31u);
-    uint32_t typ = PAT_NONE, got = 0;  // got: bit 0 transition, 1 predicted, 2 correct
-    if (i < n) {
-      const uint32_t c = a.v.sc_call[i];
-      const uint32_t s = a.v.call_sess[c];
-      if (a.role[s] == 2) {
-        const uint32_t x = a.label[c];
-        if (x >= a.L) {
-          bad_label(a, c);
-        } else {
-          const uint32_t y = succ_of(a, i, c, s);
-          if (y != PAT_NONE && y <= a.L) {
-            typ = a.v.styp[s];
-            const uint32_t p = a.pred[typ * a.L + x];
-            got = 1u | (p != PAT_NONE ? 2u : 0u) | (p == y ? 4u : 0u);
-          }
-        }
-      }
+  for_each_transition(a, 2, [&](uint32_t typ, uint32_t x, uint32_t y) {
+    uint32_t got = 0;  // bit 0 transition, 1 predicted, 2 correct (typ is warp-uniform)
+    if (x != PAT_NONE) {
+      const uint32_t p = a.pred[typ * a.L + x];
+      got = 1u | (p != PAT_NONE ? 2u : 0u) | (p == y ? 4u : 0u);
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, typ);
-    const uint32_t nt = __popc(__ballot_sync(0xffffffffu, got & 1u) & peers);
-    const uint32_t np = __popc(__ballot_sync(0xffffffffu, (got >> 1) & 1u) & peers);
-    const uint32_t nc = __popc(__ballot_sync(0xffffffffu, (got >> 2) & 1u) & peers);
-    if (typ != PAT_NONE && (int)(threadIdx.x & 31u) == __ffs(peers) - 1) {
+    const uint32_t nt = __popc(__ballot_sync(0xffffffffu, got & 1u));
+    const uint32_t np = __popc(__ballot_sync(0xffffffffu, (got >> 1) & 1u));
+    const uint32_t nc = __popc(__ballot_sync(0xffffffffu, (got >> 2) & 1u));
+    if ((threadIdx.x & 31u) == 0 && nt) {
       atomicAdd(&s_ev[typ * 3 + 0], (unsigned long long)nt);
       if (np) atomicAdd(&s_ev[typ * 3 + 1], (unsigned long long)np);
       if (nc) atomicAdd(&s_ev[typ * 3 + 2], (unsigned long long)nc);
     }
-  }
+  });
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < a.v.n_types * 3; b += PT)
     if (s_ev[b]) atomicAdd(&a.eval[(b / 3) * 4 + (b % 3)], s_ev[b]);
@@ -177,8 +163,8 @@ saga_status run_pattern(const saga_trace* t, const uint32_t* label, uint32_t L, 
   SAGA_CK(cudaMemsetAsync(counts, 0, (size_t)a.bins * 8, s));
   SAGA_CK(cudaMemsetAsync(tasks, 0, (size_t)v.n_types * 4, s));
   if (eval) SAGA_CK(cudaMemsetAsync(eval, 0, (size_t)v.n_types * 32, s));
-  // one wave of resident CTAs (8 per SM), grid-stride over the call list
-  const uint64_t want = ((uint64_t)v.n_calls + PT - 1) / PT;
+  // one warp per session, at most one wave of resident CTAs (8 per SM)
+  const uint64_t want = ((uint64_t)v.n_sessions * 32 + PT - 1) / PT;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 8ull));
   prof_begin(SAGA_PROF_PATTERN, s);
   if (a.bins <= SMEM_BINS) k_pat_count<true><<<grid, PT, a.bins * 4, s>>>(a);
