@@ -342,6 +342,9 @@ def main():
     dev_keep = []
     dptrs = []
     for name, dt in saga.DESC_ARRAYS:
+        if name in saga.OPTIONAL_ARRAYS and getattr(desc, name, None) is None:
+            dptrs.append(None)
+            continue
         a = np.ascontiguousarray(getattr(desc, name), dtype=dt)
         t = torch.from_numpy(a.view(np.uint8).copy() if a.size else np.zeros(1, np.uint8)).to(dev)
         dev_keep.append(t)

@@ -91,6 +91,9 @@ class TraceDesc:
     # generator metadata, not part of saga_trace_desc: tool type phi(v) of each AEG node, the label
     # a request stream exposes (F3); index into TOOL_LABELS
     node_tool: Optional[np.ndarray] = None
+    # optional per-call overrides of the node TTL base / observation length (saga_trace_desc)
+    call_ttl_base_us: Optional[np.ndarray] = None
+    call_obs_tokens: Optional[np.ndarray] = None
 
     @property
     def n_calls(self):

@@ -119,6 +119,12 @@ typedef struct {
   const uint8_t* node_terminal;       /* [n_aeg_nodes] terminal node                          */
   const uint32_t* type_shared_lo;     /* [n_types] shared-prefix span of the agent type        */
   const uint32_t* type_shared_len;
+  /* Optional per-call overrides (NULL = the call's AEG node values), e.g. the online statistics
+   * of saga_tool_stats (F4): call_ttl_base_us replaces node_ttl_base_us[v_c] wherever call c's
+   * TTL base is read (placement's cached(w,s), the Alg. 1 protection of its session's blocks),
+   * in [0, 1e9]; call_obs_tokens replaces node_obs_tokens[v_c] in eq:overlap. */
+  const int64_t* call_ttl_base_us;    /* [n_calls] or NULL */
+  const uint32_t* call_obs_tokens;    /* [n_calls] or NULL */
 } saga_trace_desc;
 
 /* Placement configuration (DESIGN.md R-load, R-steal): 100 ms epochs, kappa
@@ -273,6 +279,28 @@ saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_
  * Integer outputs are exact.  SAGA_ERR_INVALID_ARG for a label >= n_labels (checked on the
  * device; syncs once at the end) or arguments out of range. */
 enum { SAGA_PATTERN_NONE = 0xFFFFFFFFu };
+
+/* F4, online tool statistics: the per-call TTL base of Alg. 1 line 2
+ * ("ttl_base <- Percentile(H_t, p)") and the expected observation length of
+ * eq:overlap ("tool-type-specific distributions maintained via exponential moving averages",
+ * P:685), from the history the trace itself reveals.  Readings R-online in DESIGN.md §3.
+ *   A sample of tool x: a call d labelled x with a successor d' in its session; latency
+ *   t(d') - t_end(d) clamped to [0, 2^32 - 1] (t_end = tool start, A1), observation
+ *   call_new_tokens[d'], completed at t(d').  For call c (tool x = call_label[c]) the history H is
+ *   the samples of x completed at or before t_end(c), in completion (trace) order; k = |H|.
+ *   ttl_out_dev[c] (int64) = the nearest-rank p_pm/1000 percentile of the latencies of the last
+ *     min(k, window) samples (ascending, rank ceil(p_pm n / 1000)), capped at 1e9; the node's
+ *     node_ttl_base_us when fewer than min_samples (cold start).
+ *   obs_out_dev[c] (uint32) = floor(E + 0.5), E = the alpha = 0.2 EMA started at the node's
+ *     node_obs_tokens and truncated to the newest ema_terms samples:
+ *     E = [k <= ema_terms] 0.8^k n0 + sum_{i = m-1 .. 0} (0.2 0.8^i) obs_{k-1-i}, m = min(k, ema_terms),
+ *     evaluated in fp64 in that order (weights by repeated multiplication, no contraction).
+ * Labels as saga_pattern_infer (n_labels <= 64); 1 <= window <= 1024; ema_terms <= 256.  Both
+ * outputs are exact (integer results of pinned fp64 arithmetic).  Feed them back through
+ * saga_trace_desc.call_ttl_base_us / call_obs_tokens.  Syncs once (label check). */
+saga_status saga_tool_stats(const saga_trace* t, const uint32_t* call_label_dev, uint32_t n_labels, uint32_t p_pm,
+                            uint32_t window, uint32_t min_samples, uint32_t ema_terms, int64_t* ttl_out_dev,
+                            uint32_t* obs_out_dev, saga_stream_t stream);
 saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_dev, uint32_t n_labels,
                                const uint8_t* session_role_dev, uint32_t theta_pm, uint32_t min_tasks,
                                uint64_t* counts_dev, uint32_t* tasks_dev, uint32_t* pred_dev, float* prob_dev,

@@ -46,7 +46,7 @@ class ODesc(C.Structure):
         ("session_block_len", C.c_void_p), ("aeg_edge_off", C.c_void_p), ("edge_dst", C.c_void_p),
         ("edge_p", C.c_void_p), ("edge_shared_q16", C.c_void_p), ("node_ttl_base_us", C.c_void_p),
         ("node_obs_tokens", C.c_void_p), ("node_terminal", C.c_void_p), ("type_shared_lo", C.c_void_p),
-        ("type_shared_len", C.c_void_p)]
+        ("type_shared_len", C.c_void_p), ("call_ttl_base_us", C.c_void_p), ("call_obs_tokens", C.c_void_p)]
 
 
 class OPlace(C.Structure):
@@ -121,8 +121,8 @@ class Oracle:
         self._keep = {}
         arrs = {}
         for f, _ in ODesc._fields_[9:]:
-            a = np.ascontiguousarray(getattr(desc, f))
-            arrs[f] = a
+            a = getattr(desc, f, None)  # the per-call overrides are optional
+            arrs[f] = None if a is None else np.ascontiguousarray(a)
         self._keep = arrs
         d = ODesc(desc.n_calls, desc.n_sessions, desc.n_types, desc.n_aeg_nodes, desc.n_edges, desc.n_ranges,
                   desc.n_blocks, desc.n_nodes, desc.block_tokens, *[_p(arrs[f]) for f, _ in ODesc._fields_[9:]])

@@ -62,6 +62,8 @@ struct ODesc {
   const uint8_t* node_terminal;
   const uint32_t* type_shared_lo;
   const uint32_t* type_shared_len;
+  const int64_t* call_ttl_base_us;   // optional per-call overrides (NULL = node values)
+  const uint32_t* call_obs_tokens;
 };
 struct OPlace {
   int64_t epoch_us;
@@ -134,6 +136,11 @@ struct Oracle {
   std::vector<uint16_t> styp;
   std::vector<float> ep;
   std::vector<int64_t> ttl;
+  std::vector<int64_t> cttl;          // optional per-call TTL base (empty = node values)
+  std::vector<uint32_t> cobs;         // optional per-call expected observation length
+  // TTL base / expected observation length of call c (per-call override, else its node's value)
+  int64_t ttl_of(uint32_t c) const { return cttl.empty() ? ttl[vnode[c]] : cttl[c]; }
+  uint32_t obs_of(uint32_t c) const { return cobs.empty() ? obs[vnode[c]] : cobs[c]; }
   OPlace pc;
   // ---- derived ----
   std::vector<uint32_t> owner;        // owner[b]: session id, or n_sessions + type for shared prefix
@@ -197,6 +204,8 @@ struct Oracle {
       if (sum > 1.0 + 1e-6) return 21;
       if (ttl[v] < 0 || ttl[v] > 1000000000) return 22;
     }
+    for (int64_t x : cttl)
+      if (x < 0 || x > 1000000000) return 22;
     return 0;
   }
 
@@ -289,7 +298,7 @@ struct Oracle {
         bool cached = false;
         if (ws >= 0) {
           uint32_t lv = vnode[last_c[s]];
-          cached = !term[lv] && (Te - t_end(uint32_t(last_c[s])) <= ttl[lv]);   // Alg. 1 with m = 0
+          cached = !term[lv] && (Te - t_end(uint32_t(last_c[s])) <= ttl_of(uint32_t(last_c[s])));   // Alg. 1 with m = 0
         }
         uint32_t w;
         if (cached && 1000 * load(uint32_t(ws)) < int64_t(pc.theta_pm) * K * E) {
@@ -485,13 +494,13 @@ struct Oracle {
     uint32_t v = vnode[c];
     st.fin = last[c] || term[v];
     st.t_call = t_end(uint32_t(c));          // tool start of c* (Alg. 1 elapsed time)
-    st.ttl_base = ttl[v];
+    st.ttl_base = ttl_of(uint32_t(c));
     float P = 0.0f;
     double P64 = 0.0;
     if (!st.fin) {
       for (uint32_t k = eoff[v]; k < eoff[v + 1]; ++k) {              // eq:reuse: sum_u P(v->u) overlap(s,u)
         uint64_t nsh = (ncur * uint64_t(eq16[k])) >> 16;             // per-branch shared prefix
-        uint64_t den = ncur + obs[v];
+        uint64_t den = ncur + obs_of(uint32_t(c));
         float ov = den == 0 ? 1.0f : float(int64_t(nsh)) / float(int64_t(den));   // n_cur/(n_cur+n_obs)
         double ov64 = den == 0 ? 1.0 : double(nsh) / double(den);
         P = P + ep[k] * ov;
@@ -689,6 +698,8 @@ Oracle* build(const ODesc* d, const OPlace* p, int* err) {
   o->ttl = cp(d->node_ttl_base_us, d->n_aeg_nodes); o->obs = cp(d->node_obs_tokens, d->n_aeg_nodes);
   o->term = cp(d->node_terminal, d->n_aeg_nodes); o->tlo = cp(d->type_shared_lo, d->n_types);
   o->tlen = cp(d->type_shared_len, d->n_types);
+  if (d->call_ttl_base_us) o->cttl = cp(d->call_ttl_base_us, d->n_calls);
+  if (d->call_obs_tokens) o->cobs = cp(d->call_obs_tokens, d->n_calls);
   o->pc = *p;
   if (p->epoch_us <= 0 || p->kappa == 0 || p->prefill_tok_s == 0 || p->decode_tok_s == 0) { *err = 100; delete o; return nullptr; }
   int v = o->validate();

@@ -34,6 +34,7 @@ __global__ void k_validate_calls(TraceView v, VErr* err) {
       if (!(tp < t || (tp == t && sp < s))) fail(err, V_CALL_ORDER, c);
     }
     if (s >= v.n_sessions || v.call_v[c] >= v.n_aeg) { fail(err, V_CALL_IDS, c); continue; }
+    if (v.cttl && (v.cttl[c] < 0 || v.cttl[c] > 1000000000ll)) fail(err, V_TTL, c);
     uint32_t pr = v.call_prompt[c];
     if (pr < 1 || v.call_new[c] > pr) fail(err, V_TOKENS, c);
     int64_t work = ceil_div64(int64_t(pr) * 1000000, v.prefill_tok_s) +
@@ -114,7 +115,7 @@ __global__ void k_call_derived(TraceView v, uint32_t* ecall, int64_t* tend, uint
     if (!fin) {
       for (uint32_t e = v.eoff[x]; e < v.eoff[x + 1]; ++e) {
         uint64_t nsh = (ncur * uint64_t(v.eq16[e])) >> 16;
-        uint64_t den = ncur + v.obs[x];
+        uint64_t den = ncur + call_obs(v, c);
         float ov = den == 0 ? 1.0f : __fdiv_rn(__ll2float_rn((long long)nsh), __ll2float_rn((long long)den));
         P = __fadd_rn(P, __fmul_rn(v.ep[e], ov));
       }
@@ -220,6 +221,8 @@ saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d) {
   UP(type_shared_lo, d->n_types, tlo);
   UP(type_shared_len, d->n_types, tlen);
 #undef UP
+  if (d->call_ttl_base_us && (st = upload(t, d->call_ttl_base_us, d->n_calls, &v.cttl, true)) != SAGA_OK) return st;
+  if (d->call_obs_tokens && (st = upload(t, d->call_obs_tokens, d->n_calls, &v.cobs, true)) != SAGA_OK) return st;
   VErr* err = dalloc<VErr>(t, 1);
   uint32_t* owner = dalloc<uint32_t>(t, d->n_blocks);
   if (!err || !owner) { set_error("saga_load_trace: out of device memory"); return SAGA_ERR_OOM; }

@@ -66,7 +66,7 @@ __global__ void k_call_rec(TraceView v, CallRec* rec) {
     r.om_full = (uint32_t)(ceil_div64((int64_t)v.call_prompt[c] * 1000000, v.prefill_tok_s) + dec);
     const bool term = v.term[vc] != 0;
     r.tyf = (uint32_t)v.styp[s] | ((v.call_last[c] || term) ? F_FNEW : 0u) | (term ? F_TERM : 0u);
-    r.ttl = (uint32_t)v.ttl[vc];
+    r.ttl = (uint32_t)call_ttl_base(v, c);  // per-call override or the node's value
     r.tend = v.tend[c];
     rec[c] = r;
   }

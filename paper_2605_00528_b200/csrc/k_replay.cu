@@ -1047,7 +1047,7 @@ __global__ void k_call_key(TraceView v, CallKey* ck) {
     k.tend = v.tend[c];
     k.P = v.ci_P[c];
     k.size = v.ci_size[c];
-    k.ttl = (uint32_t)v.ttl[v.call_v[c]];
+    k.ttl = (uint32_t)call_ttl_base(v, c);
     k.fin = v.ci_fin[c];
     ck[c] = k;
   }

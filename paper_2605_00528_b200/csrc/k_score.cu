@@ -59,7 +59,7 @@ __device__ __forceinline__ OwnerKeyIn owner_at(const TraceView& v, uint32_t o, u
   r.fin = __ldg(&v.ci_fin[c]) != 0;
   r.P = __ldg(&v.ci_P[c]);
   r.t_call = __ldg(&v.tend[c]);
-  r.ttl_base = __ldg(&v.ttl[__ldg(&v.call_v[c])]);
+  r.ttl_base = call_ttl_base(v, c);
   return r;
 }
 

@@ -449,6 +449,26 @@ saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_d
   return SAGA_OK;
 }
 
+saga_status saga_tool_stats(const saga_trace* t, const uint32_t* call_label_dev, uint32_t n_labels, uint32_t p_pm,
+                            uint32_t window, uint32_t min_samples, uint32_t ema_terms, int64_t* ttl_out_dev,
+                            uint32_t* obs_out_dev, saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if ((t->n_calls && (!call_label_dev || !ttl_out_dev || !obs_out_dev))) {
+    set_error("saga_tool_stats: NULL argument");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  if (n_labels == 0 || n_labels > 64 || p_pm == 0 || p_pm > 1000 || window == 0 || window > 1024 || ema_terms > 256) {
+    set_error("saga_tool_stats: need 1 <= n_labels <= 64, 1 <= p_pm <= 1000, 1 <= window <= 1024, ema_terms <= 256");
+    return SAGA_ERR_INVALID_ARG;
+  }
+  SAGA_CK(cudaSetDevice(t->device));
+  const cudaStream_t s = stream ? (cudaStream_t)stream : t->stream;
+  GUARD(const_cast<saga_trace*>(t), join(t->stream, s));
+  GUARD(const_cast<saga_trace*>(t), run_tool_stats(t, call_label_dev, n_labels, p_pm, window, min_samples, ema_terms,
+                                                   ttl_out_dev, obs_out_dev, s));
+  return SAGA_OK;
+}
+
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream) {
   CHECK_HANDLE(t);

@@ -81,6 +81,8 @@ struct TraceView {
   const uint8_t* term;
   const uint32_t* tlo;
   const uint32_t* tlen;
+  const int64_t* cttl = nullptr;   // optional per-call TTL base (overrides ttl[call_v[c]])
+  const uint32_t* cobs = nullptr;  // optional per-call expected observation length
   // derived (A1)
   const uint32_t* ecall;   // admission epoch e(c) = t/E + 1
   const int64_t* tend;     // tool start t_c + prefill(new) + decode(out)
@@ -181,6 +183,14 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 }
 
 __host__ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// TTL base / expected observation length of call c: the per-call override when given, else the
+// value of its AEG node
+__device__ __forceinline__ int64_t call_ttl_base(const TraceView& v, uint32_t c) {
+  return v.cttl ? v.cttl[c] : v.ttl[v.call_v[c]];
+}
+__device__ __forceinline__ uint32_t call_obs(const TraceView& v, uint32_t c) {
+  return v.cobs ? v.cobs[c] : v.obs[v.call_v[c]];
+}
 
 // ---- 1-D TMA bulk copies (cp.async.bulk) global -> shared, completed on an mbarrier ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -273,6 +283,8 @@ saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint3
                        const uint64_t* out_off, uint32_t* victim, cudaStream_t s);
 saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                        const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s);
+saga_status run_tool_stats(const saga_trace* t, const uint32_t* label, uint32_t n_labels, uint32_t p_pm, uint32_t window,
+                           uint32_t min_samples, uint32_t terms, int64_t* ttl_out, uint32_t* obs_out, cudaStream_t s);
 saga_status run_pattern(const saga_trace* t, const uint32_t* label, uint32_t n_labels, const uint8_t* role,
                         uint32_t theta_pm, uint32_t min_tasks, uint64_t* counts, uint32_t* tasks, uint32_t* pred,
                         float* prob, uint64_t* eval, cudaStream_t s);

@@ -29,7 +29,10 @@ DESC_ARRAYS = [("call_t_us", np.int64), ("call_session", np.uint32), ("call_aeg_
                ("session_block_len", np.uint32), ("aeg_edge_off", np.uint32), ("edge_dst", np.uint32),
                ("edge_p", np.float32), ("edge_shared_q16", np.uint32), ("node_ttl_base_us", np.int64),
                ("node_obs_tokens", np.uint32), ("node_terminal", np.uint8), ("type_shared_lo", np.uint32),
-               ("type_shared_len", np.uint32)]
+               ("type_shared_len", np.uint32),
+               # optional per-call overrides (None = the AEG node values)
+               ("call_ttl_base_us", np.int64), ("call_obs_tokens", np.uint32)]
+OPTIONAL_ARRAYS = {"call_ttl_base_us", "call_obs_tokens"}
 
 
 class SagaError(RuntimeError):
@@ -81,6 +84,7 @@ def _load():
         "saga_evict_select": (i32, [vp, vp, vp, u32, vp, vp, vp]),
         "saga_replay": (i32, [vp, C.POINTER(ReplayCfgC), vp, u32, vp, u32, vp, vp]),
         "saga_pattern_infer": (i32, [vp, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp, vp]),
+        "saga_tool_stats": (i32, [vp, vp, u32, u32, u32, u32, u32, vp, vp, vp]),
         "saga_comm_unique_id": (i32, [vp]),
         "saga_comm_init": (i32, [vp, i32, i32, i32, C.POINTER(vp)]),
         "saga_allreduce_counters": (i32, [vp, vp, C.c_size_t, i32, vp]),
@@ -133,6 +137,9 @@ class HostDesc:
         self.keep = []
         ptrs = []
         for name, dt in DESC_ARRAYS:
+            if name in OPTIONAL_ARRAYS and getattr(desc, name, None) is None:
+                ptrs.append(None)
+                continue
             a = np.ascontiguousarray(getattr(desc, name), dtype=dt)
             if pinned:
                 t = torch.from_numpy(a.view(np.uint8) if a.size else np.zeros(1, np.uint8)).pin_memory()
@@ -245,6 +252,18 @@ class Trace:
                                       ptr("counts"), ptr("tasks"), ptr("pred"), ptr("prob"), ptr("eval"),
                                       _stream_ptr(self.stream)))
         return out
+
+    def tool_stats(self, label, n_labels: int, p_pm: int = 950, window: int = 256, min_samples: int = 20,
+                   ema_terms: int = 64):
+        """F4 (saga_tool_stats): label int32 cuda tensor [n_calls].  Returns (ttl int64 [n_calls],
+        obs int32 [n_calls] (uint32 bits)) cuda tensors."""
+        import torch
+        n = self.desc.n_calls
+        ttl = torch.empty(max(n, 1), dtype=torch.int64, device=label.device)
+        obs = torch.empty(max(n, 1), dtype=torch.int32, device=label.device)
+        _check(lib.saga_tool_stats(self.h, label.data_ptr(), int(n_labels), int(p_pm), int(window), int(min_samples),
+                                   int(ema_terms), ttl.data_ptr(), obs.data_ptr(), _stream_ptr(self.stream)))
+        return ttl[:n], obs[:n]
 
     def aeg_score(self, batch: dict, rcfg: dict, key_out, score_out=None, policy=POLICY_AEG):
         """batch: dict of int/uint torch tensors seg_node, seg_epoch, seg_occ, seg_cap, seg_act (int32),
