@@ -16,7 +16,7 @@ INCLUDE = os.path.join(ROOT, "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
-                "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
+                "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"] + os.environ.get("SAGA_NVCC_EXTRA", "").split()
 
 
 def _stale(target, deps):
@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        if force or _stale(o, [s] + hdrs):
+        deps = [s] + hdrs + ([os.path.join(CSRC, "k_replay.cu")] if s.endswith("k_replay_wide.cu") else [])
+        if force or _stale(o, deps):
             jobs.append([NVCC] + FLAGS + ["-c", s, "-o", o])
 
     def run(cmd):

@@ -37,7 +37,24 @@
 namespace saga {
 namespace {
 
-constexpr int RT = 512;
+// CTA shape (overridable at build time for occupancy experiments: SAGA_NVCC_EXTRA="-DSAGA_REPLAY_RT=256 ...")
+#ifndef SAGA_REPLAY_RT
+#define SAGA_REPLAY_RT 512
+#endif
+#ifndef SAGA_REPLAY_MINB
+#define SAGA_REPLAY_MINB 1
+#endif
+#ifndef SAGA_REPLAY_PF
+#define SAGA_REPLAY_PF 2048
+#endif
+#ifndef SAGA_REPLAY_DYN_KB
+#define SAGA_REPLAY_DYN_KB 64
+#endif
+#ifndef SAGA_REPLAY_ENTRY
+#define SAGA_REPLAY_ENTRY run_replay
+#define SAGA_REPLAY_IS_WIDE 0
+#endif
+constexpr int RT = SAGA_REPLAY_RT;
 constexpr int RW = RT / 32;
 constexpr uint32_t KIND_MIG = 0x80000000u;  // u_of bit 31: the position is a MIG record
 constexpr uint32_t U_SHARED = 0x40000000u;  // u_of bit 30: the block is a shared-prefix block
@@ -144,7 +161,7 @@ struct Smem {
 
 // Per-position arrays of an epoch (lidf, u_of, nxt, prv, upu) are staged in shared memory by TMA
 // bulk copies one epoch ahead: PF positions per array and stage, two stages.
-constexpr uint32_t PF = 2048;
+constexpr uint32_t PF = SAGA_REPLAY_PF;
 constexpr uint32_t NPA = 5;
 constexpr uint32_t PF_WORDS = 2 * NPA * PF;
 
@@ -424,7 +441,7 @@ __device__ __forceinline__ uint32_t unit_mask(uint32_t wi, uint32_t pa, uint32_t
   return m;
 }
 
-__global__ void __launch_bounds__(RT) k_replay(ReplayArgs a) {
+__global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
   __shared__ Smem sm;
   __shared__ long long s_ctr[SAGA_NCOUNT];
   extern __shared__ __align__(16) uint32_t dyn_all[];
@@ -1227,7 +1244,14 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
 
 }  // namespace
 
-saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
+#if !SAGA_REPLAY_IS_WIDE
+// k_replay_wide.cu: the same kernel at 256 threads x 2 CTAs per SM for launches of more items
+// than SMs (DESIGN.md §6 "Replay occupancy")
+saga_status run_replay_wide(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
+                            const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s);
+#endif
+
+saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                        const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s) {
   const TraceView& v = t->v;
   uint32_t pol[5], n_pol = 0;
@@ -1275,6 +1299,19 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
     for (uint32_t pi = 0; pi < n_pol; ++pi)
       for (uint32_t ni = 0; ni < n_owned; ++ni) items.push_back((pi << 28) | (ci << 12) | ni);
   const uint32_t n_items = (uint32_t)items.size();
+#if !SAGA_REPLAY_IS_WIDE
+  {
+    // one item per CTA at 512 threads is fastest while the items fit the SMs once; beyond that,
+    // two 256-thread CTAs per SM overlap two items' barrier / latency chains (C4: -24 %).
+    // SAGA_REPLAY_WIDE=1 / 0 forces either variant (parity tests run both).
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const char* f = getenv("SAGA_REPLAY_WIDE");
+    const bool wide = f ? (f[0] == '1') : (n_items > (uint32_t)nsm);
+    if (wide) return run_replay_wide(t, cfg, caps, n_caps, nodes, n_owned, counters, s);
+  }
+#endif
   // per-CTA scratch layout (all offsets 256-byte aligned)
   auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
   const uint64_t n2N = std::max<uint64_t>(1, (maxN + (1u << 20) - 1) >> 20);
@@ -1306,7 +1343,7 @@ saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t
   //   BELADY: c2 counts of both bitmaps, then their c1 counts, then the dead bits, while they fit;
   //   AEG / EVICT_ALL: the newest-call table, then the unit counts, while they fit.
   // the rest of the 228 KB unified L1/shared array stays L1 cache, which the per-event loads need
-  uint64_t dyn_max = 64ull * 1024;
+  uint64_t dyn_max = (uint64_t)SAGA_REPLAY_DYN_KB * 1024;
   if (const char* e = getenv("SAGA_REPLAY_SMEM_KB")) dyn_max = std::max<uint64_t>(1, strtoull(e, nullptr, 10)) * 1024;
   dyn_max = std::min<uint64_t>(dyn_max, 200ull * 1024);
   const uint64_t c2_bytes = ((std::max(n2N + n2L, n2R) + 3) & ~3ull) * 4;

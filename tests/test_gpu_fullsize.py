@@ -80,6 +80,7 @@ def test_c2_full_size_equals_oracle():
 
 @pytest.mark.parametrize("name", ["C3", "C4"])
 def test_full_size_properties_and_sampled_node(name):
+    """C3 (288 items) and C4 (1,024 items) launch more items than SMs: the 256 x 2 replay shape."""
     d, pc, t, caps, ctr = _run(name)
     _properties(d, t, caps, ctr)
     o = O.Oracle(d, pc)

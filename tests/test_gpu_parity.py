@@ -106,7 +106,11 @@ def _caps_for(o, d, name):
     return sorted(set(c for c in caps if c > 0))
 
 
-def test_replay_counters_equal(pair):
+@pytest.mark.parametrize("variant", ["narrow", "wide"])
+def test_replay_counters_equal(pair, variant, monkeypatch):
+    """Both compiled shapes of the replay kernel (512 threads x 1 CTA/SM, 256 x 2; run_replay
+    picks by item count, SAGA_REPLAY_WIDE forces one) against the oracle."""
+    monkeypatch.setenv("SAGA_REPLAY_WIDE", "1" if variant == "wide" else "0")
     name, d, pc, o, t = pair
     caps = _caps_for(o, d, name)
     # AEG, BELADY, EVICT_ALL and the tab:competitive baselines LRU, LRU + Prefix
