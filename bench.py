@@ -297,7 +297,7 @@ def main():
     ap.add_argument("--no-bulk", action="store_true")
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
     ap.add_argument("--inflight", type=int, default=None,
-                    help="independent steps in flight on separate streams (default 2; 1 for C4/C5)")
+                    help="independent steps in flight on separate streams (default 2)")
     ap.add_argument("--policy-mask", type=int, default=3,
                     help="1 AEG, 2 BELADY, 4 EVICT_ALL, 8 LRU, 16 LRU+Prefix (default 3: the metric's pair)")
     args = ap.parse_args()
@@ -330,7 +330,7 @@ def main():
     rcfg = dict(policy_mask=args.policy_mask)
     caps_fn = sweep_for(args.config)
     shard_caps = (not trials) and desc.n_nodes == 1 and world > 1
-    inflight = max(1, args.inflight or (2 if desc.n_calls < 1_000_000 else 1))
+    inflight = max(1, args.inflight or 2)
     # one stream, trace handle and communicator per in-flight step (see run_steps)
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
     comm = comms[0]
@@ -369,8 +369,9 @@ def main():
 
     def step(host, i=0, j=None):
         """One step on stream i.  With steps in flight (j = step index), step j's expansion,
-        next use and replay start on the device after step j-1's replay, while its placement (a
-        single warp on one SM) runs beside that replay.  Every step does all of its work."""
+        next use and replay start after step j-1's trace was replayed and freed (so at most one
+        expanded trace is resident: C5's is ~90 GB), while its load and placement (a single warp
+        on one SM) run beside that replay.  Every step does all of its work."""
         s_ = streams[i]
         before = after = None
         if j is not None and inflight > 1:
@@ -378,19 +379,20 @@ def main():
                 if j == 0:
                     return
                 with order["cv"]:
-                    order["cv"].wait_for(lambda: (j - 1) in order["done"])
+                    order["cv"].wait_for(lambda: (j - 1) in order["done"] or order.get("error"))
+                    if order.get("error"):
+                        raise RuntimeError("another in-flight step failed")
                     ev = order["done"][j - 1]
                 mark(st, "placed", j)
-                st.wait_event(ev)
+                if ev is not None:
+                    st.wait_event(ev)
                 mark(st, "go", j)
 
             def after(st):
                 mark(st, "replayed", j)
                 ev = torch.cuda.Event()
                 ev.record(st)
-                with order["cv"]:
-                    order["done"][j] = ev
-                    order["cv"].notify_all()
+                order["ev"][j] = ev  # published once the trace is freed (run_steps.worker)
         mark(s_, "start", j)
         with torch.cuda.stream(s_):
             t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=p_rank, world=p_world,
@@ -410,6 +412,8 @@ def main():
         import concurrent.futures as cf
         with order["cv"]:
             order["done"] = {}
+            order["ev"] = {}
+            order["error"] = None
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(streams[0])
@@ -420,12 +424,21 @@ def main():
         def worker(i):
             torch.cuda.set_device(local)
             last = None
-            for j in range(i, k, inflight):
-                t, caps, ctr = step(host, i, j)
-                if d2h is not None:
-                    d2h(i, ctr)
-                t.free()
-                last = (caps, ctr)
+            try:
+                for j in range(i, k, inflight):
+                    t, caps, ctr = step(host, i, j)
+                    if d2h is not None:
+                        d2h(i, ctr)
+                    t.free()
+                    with order["cv"]:  # step j's trace is gone: step j+1 may expand
+                        order["done"][j] = order["ev"].get(j)
+                        order["cv"].notify_all()
+                    last = (caps, ctr)
+            except BaseException as exc:  # wake the other stream's thread instead of leaving it waiting
+                with order["cv"]:
+                    order["error"] = exc
+                    order["cv"].notify_all()
+                raise
             return last
 
         if inflight == 1:

@@ -60,7 +60,7 @@ void prof_end(int cat, cudaStream_t s) {
 
 // ---------------- workspace cache ----------------
 namespace ws_detail {
-struct Blk { void* p; size_t size; int dev; cudaStream_t s; bool used; };
+struct Blk { void* p; size_t size; int dev; cudaStream_t s; bool used; bool any; };  // any: stream drained
 std::mutex g_ws_mu;
 std::vector<Blk> g_ws;
 }  // namespace ws_detail
@@ -77,10 +77,10 @@ cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s) {
     size_t best = SIZE_MAX, bi = 0;
     for (size_t i = 0; i < g_ws.size(); ++i) {
       const Blk& b = g_ws[i];
-      if (b.used || b.dev != dev || b.s != s || b.size < want || b.size > 2 * want + gran) continue;
+      if (b.used || b.dev != dev || (b.s != s && !b.any) || b.size < want || b.size > 2 * want + gran) continue;
       if (b.size < best) { best = b.size; bi = i; }
     }
-    if (best != SIZE_MAX) { g_ws[bi].used = true; *p = g_ws[bi].p; return cudaSuccess; }
+    if (best != SIZE_MAX) { g_ws[bi].used = true; g_ws[bi].s = s; g_ws[bi].any = false; *p = g_ws[bi].p; return cudaSuccess; }
   }
   void* q = nullptr;
   cudaError_t e = cudaMalloc(&q, want);
@@ -100,7 +100,7 @@ cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   std::lock_guard<std::mutex> g(g_ws_mu);
-  g_ws.push_back({q, want, dev, s, true});
+  g_ws.push_back({q, want, dev, s, true, false});
   *p = q;
   return cudaSuccess;
 }
@@ -111,7 +111,15 @@ void ws_free(void* p, cudaStream_t s) {
   if (!p) return;
   std::lock_guard<std::mutex> g(g_ws_mu);
   for (Blk& b : g_ws)
-    if (b.p == p) { b.used = false; b.s = s; return; }
+    if (b.p == p) { b.used = false; b.s = s; b.any = false; return; }
+}
+
+// after the caller synchronised stream s: its idle blocks may serve any stream
+void ws_release_stream(cudaStream_t s) {
+  using namespace ws_detail;
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  for (Blk& b : g_ws)
+    if (!b.used && b.s == s) b.any = true;
 }
 
 // pinned bounce buffers for d2h / h2d, one per concurrent caller
@@ -226,7 +234,7 @@ void saga_free_trace(saga_trace* t) {
   cudaGetDevice(&prev);
   cudaSetDevice(t->device);
   for (void* p : t->allocs) ws_free(p, t->stream);
-  cudaStreamSynchronize(t->stream);
+  if (cudaStreamSynchronize(t->stream) == cudaSuccess) ws_release_stream(t->stream);  // reusable by other streams
   cudaSetDevice(prev);
   delete t;
 }

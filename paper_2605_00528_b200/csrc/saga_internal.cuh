@@ -30,6 +30,7 @@ void set_error(const char* fmt, ...);
 // (device, stream), so the hot path never grows a memory pool inside a timed step.
 cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s);
 void ws_free(void* p, cudaStream_t s);
+void ws_release_stream(cudaStream_t s);  // after a sync of s: its idle blocks serve any stream
 
 // Small host<->device copies of the host-side control flow (sizes, flags, launch tables).  Both
 // wait for the stream first and move the bytes through a pinned bounce buffer, then wait again:
