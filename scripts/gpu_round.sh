@@ -8,7 +8,7 @@ tail -3 gpurun_out/gpu_tests.log
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; rc=$?; echo "bench exit $rc" >> gpurun_out/bench_default.log
 tail -c 400 gpurun_out/bench_default.log
 if [ $rc -eq 0 ]; then
-  ARGS="--steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+  ARGS="${NCU_ARGS:---steps 1 --warmup 3 --no-cpu-baseline --no-e2e}"
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
      python bench.py $ARGS > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches exit $?" >> gpurun_out/ncu_launches.log
   KREGEX="${KREGEX:-k_pat_count}"
