@@ -254,6 +254,17 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream);
 
+/* One (policy, capacity, node) replay of A7 that also logs its victims (SURVEY §1.2's victim
+ * logs; the sketch's SAGA_LOG_VICTIMS): cfg->policy_mask must name exactly one policy.
+ * log_dev (uint64, log_cap entries, nullable when log_cap = 0) receives every victim as
+ * (epoch << 32) | local id, epochs ascending; within an epoch the order is unspecified (the set
+ * is unique, the order of equal-epoch entries is not: sort to compare); *n_logged (host) is
+ * the number of victims, which may exceed log_cap (then only log_cap were written).
+ * counters_dev int64[n_nodes][SAGA_NCOUNT]: the node's row as saga_replay writes it.  Syncs. */
+saga_status saga_replay_victims(saga_trace* t, const saga_replay_cfg* cfg, uint32_t cap, uint32_t node,
+                                uint64_t* log_dev, uint64_t log_cap, uint64_t* n_logged, int64_t* counters_dev,
+                                saga_stream_t stream);
+
 /* F3.  Pattern-based AEG inference, observability tier (b) of §3.3 (P:645:
  * "extracting tool-type patterns, computing transition probabilities, and retaining edges
  * exceeding theta_conf = 0.7"; cold start "until 30 tasks complete") and the next-step accuracy

@@ -85,6 +85,8 @@ def lib():
             L.oracle_sweep_range.argtypes = [vp, C.c_uint32, vp, vp]
             L.oracle_replay.restype = C.c_uint64
             L.oracle_replay.argtypes = [vp, C.POINTER(OReplay), C.c_uint32, C.c_uint32, vp, vp, C.c_uint64]
+            L.oracle_replay_log.restype = C.c_uint64
+            L.oracle_replay_log.argtypes = [vp, C.POINTER(OReplay), C.c_uint32, C.c_uint32, vp, vp, C.c_uint64]
             L.oracle_replay_many.argtypes = [vp, C.POINTER(OReplay), C.c_uint32, vp, C.c_uint32, vp, C.c_uint32,
                                              vp, C.c_int]
             L.oracle_min_misses.restype = C.c_int64
@@ -207,6 +209,17 @@ class Oracle:
             return ctr, buf[:n].copy()
         lib().oracle_replay(self.h, C.byref(cfg), w, cap, ctr.ctypes.data, None, 0)
         return ctr
+
+    def replay_log(self, policy, w, cap, rcfg: dict | None = None):
+        """(counters, victims as uint64 (epoch << 32) | local id in eviction order)."""
+        cfg = replay_cfg(**(rcfg or {}))
+        cfg.policy = policy
+        ctr = np.zeros(16, np.int64)
+        cap_log = 1 << 22
+        buf = np.zeros(cap_log, np.uint64)
+        n = lib().oracle_replay_log(self.h, C.byref(cfg), w, cap, ctr.ctypes.data, buf.ctypes.data, cap_log)
+        assert n <= cap_log
+        return ctr, buf[:n].copy()
 
     def replay_many(self, policy_mask, caps, nodes=None, rcfg: dict | None = None, nthreads=None):
         cfg = replay_cfg(**(rcfg or {}))

@@ -543,7 +543,8 @@ struct Oracle {
   // ------------------------------------------------------------------------------------------
   // A7 epoch-synchronous replay R1-R4 with A5 keys and A6 top-k
   // ------------------------------------------------------------------------------------------
-  void replay(const OReplay& cfg, uint32_t w, uint32_t C, int64_t* ctr, std::vector<uint32_t>* vlog) {
+  void replay(const OReplay& cfg, uint32_t w, uint32_t C, int64_t* ctr, std::vector<uint32_t>* vlog,
+              std::vector<uint32_t>* vlog_e = nullptr) {
     next_use(w);
     const NodeData& nd = nodes[w];
     const uint32_t nl = uint32_t(nd.uniq.size());
@@ -624,6 +625,7 @@ struct Oracle {
           if (cfg.policy == POL_AEG && !(keys[i].first >> 63)) ctr[C_EVICT_PROTECTED]++;
           hash += splitmix64((uint64_t(e) << 32) | b);
           if (vlog) vlog->push_back(b);
+          if (vlog_e) vlog_e->push_back(uint32_t(e));
         }
         ctr[C_EVICTIONS] += k;
         ctr[C_EVICT_EVENTS] += 1;
@@ -811,6 +813,15 @@ uint64_t oracle_replay(void* h, const OReplay* cfg, uint32_t w, uint32_t cap, in
   o->replay(*cfg, w, cap, counters, vlog ? &log : nullptr);
   if (vlog) std::memcpy(vlog, log.data(), std::min<uint64_t>(log.size(), vlog_cap) * 4);
   return log.size();
+}
+// Victim log with epochs: out[i] = (epoch << 32) | local id, in eviction order; returns the count.
+uint64_t oracle_replay_log(void* h, const OReplay* cfg, uint32_t w, uint32_t cap, int64_t* counters, uint64_t* out,
+                           uint64_t out_cap) {
+  Oracle* o = static_cast<Oracle*>(h);
+  std::vector<uint32_t> lid, ep;
+  o->replay(*cfg, w, cap, counters, &lid, &ep);
+  for (uint64_t i = 0; i < std::min<uint64_t>(lid.size(), out_cap); ++i) out[i] = (uint64_t(ep[i]) << 32) | lid[i];
+  return lid.size();
 }
 // Many replays over a std::thread pool: out[pol_idx][cap_idx][node][16] for policies in mask order
 // (AEG, BELADY, EVICT_ALL), nodes listed in `nodes` (others left untouched).

@@ -143,6 +143,9 @@ struct ReplayArgs {
   uint32_t ocall_smem;         // AEG: newest-call table (n_lo words) in shared memory
   unsigned long long* item_cyc;  // optional per-item SM cycles (SAGA_REPLAY_TRACE)
   unsigned long long* phase_cyc; // optional [item][8] per-phase cycles of thread 0
+  unsigned long long* vlog;      // optional victim log ((epoch << 32) | lid), saga_replay_victims
+  unsigned long long* vlog_n;    // entries written (may exceed vlog_cap: the caller sees the need)
+  unsigned long long vlog_cap;
   uint32_t* work;
   uint32_t* err;
   uint32_t* dbg;  // [4] first failed invariant
@@ -439,6 +442,11 @@ __device__ __forceinline__ uint32_t unit_mask(uint32_t wi, uint32_t pa, uint32_t
   if (wi == (pa >> 5)) m &= ~((1u << (pa & 31)) - 1u);
   if (wi == ((pe - 1) >> 5) && (pe & 31)) m &= (1u << (pe & 31)) - 1u;
   return m;
+}
+
+__device__ __forceinline__ void log_victim(const ReplayArgs& a, unsigned long long x) {
+  const unsigned long long i = atomicAdd(a.vlog_n, 1ull);
+  if (i < a.vlog_cap) a.vlog[i] = x;
 }
 
 __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
@@ -901,6 +909,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
                 if (qn != INF32) atomicAnd(&nres_a[qn >> 5], ~(1u << (qn & 31)));
                 res_pos[lid] = NONE;
                 hs += splitmix64(eh | lid);
+                if (a.vlog) log_victim(a, eh | lid);
                 ++tk;
               }
               n_direct += tk;
@@ -925,6 +934,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           if (in) {
             res_pos[lid] = NONE;
             hs += splitmix64(eh | lid);
+            if (a.vlog) log_victim(a, eh | lid);
           }
         }
         const unsigned long long nvp = block_reduce<RT, unsigned long long>(
@@ -1248,11 +1258,13 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
 // k_replay_wide.cu: the same kernel at 256 threads x 2 CTAs per SM for launches of more items
 // than SMs (DESIGN.md §6 "Replay occupancy")
 saga_status run_replay_wide(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
-                            const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s);
+                            const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s,
+                            uint64_t* vlog, uint64_t vlog_cap, uint64_t* vlog_n);
 #endif
 
 saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
-                       const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s) {
+                       const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s,
+                       uint64_t* vlog, uint64_t vlog_cap, uint64_t* vlog_n) {
   const TraceView& v = t->v;
   uint32_t pol[5], n_pol = 0;
   for (uint32_t p : {1u, 2u, 4u, 8u, 16u}) if (cfg->policy_mask & p) pol[n_pol++] = p;
@@ -1309,7 +1321,7 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const char* f = getenv("SAGA_REPLAY_WIDE");
     const bool wide = f ? (f[0] == '1') : (n_items > (uint32_t)nsm);
-    if (wide) return run_replay_wide(t, cfg, caps, n_caps, nodes, n_owned, counters, s);
+    if (wide) return run_replay_wide(t, cfg, caps, n_caps, nodes, n_owned, counters, s, vlog, vlog_cap, vlog_n);
   }
 #endif
   // per-CTA scratch layout (all offsets 256-byte aligned)
@@ -1402,6 +1414,9 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   a.callkey = static_cast<const CallKey*>(t->callkey);
   a.scratch = scratch; a.work = work; a.err = work + 1; a.dbg = work + 4; a.item_cyc = d_cyc;
   a.phase_cyc = d_cyc ? d_cyc + n_items : nullptr;
+  a.vlog = reinterpret_cast<unsigned long long*>(vlog);
+  a.vlog_n = reinterpret_cast<unsigned long long*>(vlog_n);
+  a.vlog_cap = vlog_cap;
   prof_begin(SAGA_PROF_REPLAY, s);
   k_replay<<<grid, RT, dyn, s>>>(a);
   prof_end(SAGA_PROF_REPLAY, s);

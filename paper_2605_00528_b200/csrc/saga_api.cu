@@ -477,6 +477,30 @@ saga_status saga_tool_stats(const saga_trace* t, const uint32_t* call_label_dev,
   return SAGA_OK;
 }
 
+saga_status saga_replay_victims(saga_trace* t, const saga_replay_cfg* cfg, uint32_t cap, uint32_t node,
+                                uint64_t* log_dev, uint64_t log_cap, uint64_t* n_logged, int64_t* counters_dev,
+                                saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if (!cfg || !counters_dev || !n_logged || (log_cap && !log_dev)) { set_error("saga_replay_victims: NULL argument"); return SAGA_ERR_INVALID_ARG; }
+  const uint32_t pm = cfg->policy_mask & 31u;
+  if (cfg->policy_mask != pm || pm == 0 || (pm & (pm - 1))) { set_error("saga_replay_victims: exactly one policy"); return SAGA_ERR_INVALID_ARG; }
+  if (cfg->p_high_pm <= cfg->p_low_pm || cfg->p_high_pm > 1000) { set_error("saga_replay_victims: need p_low_pm < p_high_pm <= 1000"); return SAGA_ERR_INVALID_ARG; }
+  if (cap == 0 || cap > (1u << 28)) { set_error("saga_replay_victims: capacity %u out of range (1..2^28)", cap); return SAGA_ERR_CAPACITY; }
+  if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_replay_victims: node %u not owned", node); return SAGA_ERR_STATE; }
+  if (!t->nodes[node].nu_done) { set_error("saga_replay_victims: saga_belady_next_use(node %u) must run first", node); return SAGA_ERR_STATE; }
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(t, join((cudaStream_t)stream, t->stream));
+  uint64_t* cnt = nullptr;
+  SAGA_CK(ws_malloc((void**)&cnt, 8, t->stream));
+  SAGA_CK(cudaMemsetAsync(cnt, 0, 8, t->stream));
+  const saga_status st = run_replay(t, cfg, &cap, 1, &node, 1, counters_dev, t->stream, log_dev, log_cap, cnt);
+  if (st == SAGA_OK) SAGA_CK(d2h(n_logged, cnt, 8, t->stream));
+  ws_free(cnt, t->stream);
+  GUARD(t, st);
+  GUARD(t, join(t->stream, (cudaStream_t)stream));
+  return SAGA_OK;
+}
+
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream) {
   CHECK_HANDLE(t);

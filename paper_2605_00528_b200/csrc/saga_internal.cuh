@@ -282,8 +282,10 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
                       uint64_t* key, cudaStream_t s);
 saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint32_t* k, uint32_t n_seg,
                        const uint64_t* out_off, uint32_t* victim, cudaStream_t s);
+// vlog (optional, device): every victim as (epoch << 32) | local id, *vlog_n (device) entries
 saga_status run_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
-                       const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s);
+                       const uint32_t* nodes, uint32_t n_owned, int64_t* counters, cudaStream_t s,
+                       uint64_t* vlog = nullptr, uint64_t vlog_cap = 0, uint64_t* vlog_n = nullptr);
 saga_status run_tool_stats(const saga_trace* t, const uint32_t* label, uint32_t n_labels, uint32_t p_pm, uint32_t window,
                            uint32_t min_samples, uint32_t terms, int64_t* ttl_out, uint32_t* obs_out, cudaStream_t s);
 saga_status run_pattern(const saga_trace* t, const uint32_t* label, uint32_t n_labels, const uint8_t* role,

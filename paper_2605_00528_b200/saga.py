@@ -83,6 +83,7 @@ def _load():
         "saga_aeg_score": (i32, [vp, C.POINTER(ScoreBatchC), C.POINTER(ReplayCfgC), vp, vp, vp]),
         "saga_evict_select": (i32, [vp, vp, vp, u32, vp, vp, vp]),
         "saga_replay": (i32, [vp, C.POINTER(ReplayCfgC), vp, u32, vp, u32, vp, vp]),
+        "saga_replay_victims": (i32, [vp, C.POINTER(ReplayCfgC), u32, u32, vp, u64, C.POINTER(u64), vp, vp]),
         "saga_pattern_infer": (i32, [vp, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp, vp]),
         "saga_tool_stats": (i32, [vp, vp, u32, u32, u32, u32, u32, vp, vp, vp]),
         "saga_comm_unique_id": (i32, [vp]),
@@ -252,6 +253,20 @@ class Trace:
                                       ptr("counts"), ptr("tasks"), ptr("pred"), ptr("prob"), ptr("eval"),
                                       _stream_ptr(self.stream)))
         return out
+
+    def replay_victims(self, rcfg: dict, cap: int, node: int, log_cap: int = 1 << 22):
+        """One (policy, cap, node) replay with its victim log.  Returns (counters int64[16] numpy,
+        victims uint64 numpy of (epoch << 32) | local id, epochs ascending)."""
+        import torch
+        cfg = replay_cfg_c(rcfg)
+        ctr = torch.zeros((self.desc.n_nodes, NCOUNT), dtype=torch.int64, device=f"cuda:{self.device}")
+        log = torch.empty(max(1, log_cap), dtype=torch.int64, device=f"cuda:{self.device}")
+        n = C.c_uint64(0)
+        _check(lib.saga_replay_victims(self.h, C.byref(cfg), int(cap), int(node), log.data_ptr(), int(log_cap),
+                                       C.byref(n), ctr.data_ptr(), _stream_ptr(self.stream)))
+        if n.value > log_cap:
+            raise SagaError(4, f"victim log needs {n.value} entries (log_cap {log_cap})")
+        return ctr[node].cpu().numpy(), log[:n.value].cpu().numpy().view(np.uint64)
 
     def tool_stats(self, label, n_labels: int, p_pm: int = 950, window: int = 256, min_samples: int = 20,
                    ema_terms: int = 64):

@@ -292,3 +292,21 @@ def test_launches_counted():
     t = saga.Trace(make_c1(), default_place_cfg())
     t.next_use(0)
     assert saga.kernel_launches() > before
+
+
+def test_victim_log_equal(pair):
+    """saga_replay_victims: every victim of every eviction epoch, (epoch, local id) sets equal to
+    the oracle's log for each policy, node and a few capacities; epochs ascending on both sides
+    (single-item launches take the 512-thread shape; the counters test covers both shapes)."""
+    name, d, pc, o, t = pair
+    caps = _caps_for(o, d, name)
+    caps = sorted(set([caps[0], caps[len(caps) // 2], caps[-1]]))
+    for pol in (O.POL_AEG, O.POL_BELADY, O.POL_EVICT_ALL, O.POL_LRU, O.POL_LRU_PREFIX):
+        for w in range(d.n_nodes):
+            for cap in caps:
+                gc, glog = t.replay_victims(dict(policy_mask=pol), cap, w)
+                rc, rlog = o.replay_log(pol, w, cap)
+                assert np.array_equal(gc, rc), (name, pol, w, cap)
+                assert np.array_equal(np.sort(glog), np.sort(rlog)), (name, pol, w, cap)
+                ge = (glog >> np.uint64(32)).astype(np.int64)
+                assert np.all(np.diff(ge) >= 0)

@@ -503,3 +503,22 @@ def test_invalid_traces_rejected(O):
     d.range_block_lo[1] = 40  # session 0 touching session 3's blocks
     with pytest.raises(ValueError):
         O.Oracle(d, default_place_cfg())
+
+
+def test_victim_log_with_epochs(O):
+    """replay_log = replay(log=True) plus the epoch of each victim: same victims in the same order,
+    epochs non-decreasing, one entry per eviction."""
+    for seed in range(4):
+        d = make_random_small(seed, n_sessions=6, n_nodes=2, max_calls=5, max_blocks=8)
+        o = O.Oracle(d, default_place_cfg(seed))
+        for w in range(d.n_nodes):
+            lo, hi = o.sweep_range(w)
+            for C in range(max(lo, 1), hi + 2):
+                for pol in (O.POL_AEG, O.POL_BELADY, O.POL_LRU):
+                    c1, lids = o.replay(pol, w, C, log=True)
+                    c2, log = o.replay_log(pol, w, C)
+                    assert np.array_equal(c1, c2)
+                    assert [int(x) & 0xFFFFFFFF for x in log] == [int(x) for x in lids]
+                    ep = [int(x) >> 32 for x in log]
+                    assert ep == sorted(ep)
+                    assert len(log) == c1[O.CI["EVICTIONS"]]
