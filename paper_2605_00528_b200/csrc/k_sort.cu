@@ -126,7 +126,18 @@ __global__ void __launch_bounds__(SORT_T) k_onesweep(const uint32_t* __restrict_
     const uint64_t idx = wbase + (uint64_t)i * 32 + lane;
     const bool ok = idx < n;
     const uint32_t d = ok ? ((k[i] >> shift) & (RADIX - 1)) : 0x100u;
+#ifdef SAGA_SORT_MATCH_ANY
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#else
+    // lanes holding the same 9-bit value (0x100 = past the end): 9 ballots instead of MATCH
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < RBITS + 1; ++b) {
+      const uint32_t bit = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+#endif
     const uint32_t leader = 31 - __clz(peers);
     uint32_t c = 0;
     if (ok && lane == leader) {
