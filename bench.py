@@ -191,9 +191,9 @@ def f3_pattern(stream, dev, reps=5, config="C5"):
     1 x 2 passes + type 2 + sc_off 4 + call_is_last 1 = 9 B."""
     import numpy as np
     import torch
-    from gen import TOOL_LABELS, make, pattern_labels, pattern_roles, place_cfg_for
+    from gen import TOOL_LABELS, pattern_labels, pattern_roles, place_cfg_for
     from paper_2605_00528_b200 import saga
-    d = make(config)
+    d = _big_trace(config)
     t = saga.Trace(d, place_cfg_for(d), stream=stream, defer_expand=True)
     lab = torch.from_numpy(pattern_labels(d).view(np.int32)).to(dev)
     role = torch.from_numpy(pattern_roles(d)).to(dev)
@@ -226,6 +226,56 @@ def f3_pattern(stream, dev, reps=5, config="C5"):
             "held_out_accuracy": float(ev[:, 2].sum()) / max(1, int(ev[:, 0].sum())),
             "note": "ms / GB/s: device time of the three kernels (CUDA events around them); ms_call: the whole "
                     "API call incl. memsets and its one sync (label check readback)"}
+
+
+_BIG = {}
+
+
+def _big_trace(config):
+    """the generated trace of a large config, generated once per process (F3 / F4 legs)"""
+    from gen import make
+    if config not in _BIG:
+        _BIG[config] = make(config)
+    return _BIG[config]
+
+
+def f4_tool_stats(stream, dev, reps=3, config="C5"):
+    """SURVEY §8(f) F4 online statistics on the largest config (6.4 M calls): saga_tool_stats with
+    the generator's tool labels (window 256, p95, 64-term EMA).  Reports calls/s; the kernels'
+    work is dominated by the per-call window select (up to 256 latencies per call, re-read from
+    L1/L2 by consecutive calls of a tool), so no HBM fraction is claimed."""
+    import numpy as np
+    import torch
+    import ctypes as C
+    from gen import TOOL_LABELS, pattern_labels, place_cfg_for
+    from paper_2605_00528_b200 import saga
+    d = _big_trace(config)
+    t = saga.Trace(d, place_cfg_for(d), stream=stream, defer_expand=True)
+    lab = torch.from_numpy(pattern_labels(d).view(np.int32)).to(dev)
+    L = len(TOOL_LABELS)
+    with torch.cuda.stream(stream):
+        t.tool_stats(lab, L)
+        stream.synchronize()
+        saga.lib.saga_profile_enable(1)
+        saga.lib.saga_profile_read(None, None)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            ttl, obs = t.tool_stats(lab, L)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    pm = (C.c_double * len(PROF_NAMES))()
+    pn = (C.c_uint64 * len(PROF_NAMES))()
+    saga.lib.saga_profile_read(pm, pn)
+    saga.lib.saga_profile_enable(0)
+    k_ms = (pm[PROF_NAMES.index("pattern")] + pm[PROF_NAMES.index("sort")]) / reps
+    changed = float((ttl.cpu().numpy() != np.asarray(d.node_ttl_base_us)[np.asarray(d.call_aeg_node)]).mean())
+    t.free()
+    return {"config": config, "calls": d.n_calls, "ms_call": ms, "ms": k_ms, "calls_per_s": d.n_calls / (k_ms / 1e3),
+            "frac_calls_ttl_changed": changed,
+            "note": "ms: device time of the sample, sort, gather and per-call select kernels; ms_call: the API call"}
 
 
 def run_reference(args):
@@ -564,7 +614,7 @@ def main():
                 "traffic": traffic, "peak_source": peak_kind,
                 "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
 
-    bulk = pat = None
+    bulk = pat = f4 = None
     if world == 1 and not args.no_bulk:  # single process: no collective may be issued by one rank
         with torch.cuda.stream(stream):
             t_b, _, _ = pipeline.run_step(desc, pc, rcfg, caps_fn, device=local, stream=stream, host=dd)
@@ -577,6 +627,7 @@ def main():
                     kv["frac"] = kv["algorithmic_gb_s"] / peak
         pat = f3_pattern(stream, dev)
         pat["frac"] = pat["algorithmic_gb_s"] / peak
+        f4 = f4_tool_stats(stream, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(desc, pc, caps, os.cpu_count() or 1)
@@ -597,7 +648,7 @@ def main():
                        "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
                                     else ("capacity points" if shard_caps else "cache nodes w mod R"))},
             "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels, "bulk_score_select": bulk, "f3_pattern": pat,
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels, "bulk_score_select": bulk, "f3_pattern": pat, "f4_tool_stats": f4,
             "counters_checksum": int(np.bitwise_xor.reduce(counters_host.reshape(-1).view(np.uint64))),
         }
         print(json.dumps(line), flush=True)
