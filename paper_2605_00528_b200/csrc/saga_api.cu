@@ -1,6 +1,7 @@
 // C ABI of libsaga (include/saga.h): argument checks, handle lifetime, stream ordering.
 // Every compute step runs in the kernels of k_*.cu; nothing here touches trace data on the host.
 #include <cstring>
+#include <chrono>
 #include <mutex>
 
 #include "saga_internal.cuh"
@@ -83,7 +84,12 @@ cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s) {
     if (best != SIZE_MAX) { g_ws[bi].used = true; g_ws[bi].s = s; g_ws[bi].any = false; *p = g_ws[bi].p; return cudaSuccess; }
   }
   void* q = nullptr;
+  static const bool dbg = getenv("SAGA_WS_DEBUG") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMalloc(&q, want);
+  if (dbg)
+    fprintf(stderr, "[saga ws] cudaMalloc %zu B on stream %p: %.3f ms\n", want, (void*)s,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   if (e != cudaSuccess) {  // release cached idle blocks of this device and retry once
     cudaGetLastError();
     std::vector<void*> drop;
