@@ -601,10 +601,12 @@ def main():
     dom = max((k for k in kernels if k in ("sort", "segscan", "epoch_stats", "replay", "expand")),
               key=lambda k: kernels[k]["ms_per_step"], default=None)
     traffic = None
+    tinfo = {}
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if dom and os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(dom)
+            tinfo = json.load(open(tfile))
+            traffic = tinfo.get(dom)
         except Exception:
             traffic = None
     roof = None
@@ -613,6 +615,16 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "peak_source": peak_kind,
                 "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
+        inst = tinfo.get(dom + "_warp_inst") if args.config == "C2" and args.policy_mask == 3 else None
+        if inst:
+            # the replay is issue/latency-bound: its warp-instruction rate against the SM issue peak
+            # (148 SMs x 4 schedulers x 1 instruction per clock at the sampled SM clock), DESIGN.md §6
+            ms_k = kernels[dom]["ms_per_step"]
+            mhz = clocks.get("sm_mhz") or 1965.0
+            peak_i = 148 * 4 * mhz * 1e6 / 1e9
+            ach_i = inst / (ms_k / 1e3) / 1e9
+            roof["issue"] = {"achieved": ach_i, "peak": peak_i, "unit": "G warp-inst/s", "frac": ach_i / peak_i,
+                             "warp_inst_per_launch": inst, "source": "ncu smsp__inst_executed.sum of one launch"}
 
     bulk = pat = f4 = None
     if world == 1 and not args.no_bulk:  # single process: no collective may be issued by one rank
