@@ -989,8 +989,19 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       }
       S += nnew;
       PH(6);
-      // ---- live unit list: keep units with cnt > 0, append this epoch's units ----
-      if (units) {
+      // ---- live unit list: append this epoch's units; every 16th epoch also drop the units
+      // whose count reached 0 (until then the passes skip them: each one tests cnt first) ----
+      if (units && (j & 15u) != 15u) {
+        ListRec* L = lists[cur];
+        const uint32_t U0 = nd.ev_unit[j], U1 = nd.ev_unit[j + 1];
+        for (uint32_t i = threadIdx.x; i < U1 - U0; i += RT) {
+          const UnitRec ur = nd.urec[U0 + i];
+          ListRec r{};
+          r.t = ur.t; r.u = U0 + i; r.pa = ur.pa; r.pe = ur.pe; r.lo = ur.lo; r.kp = 0; r.flags = ur.flags;
+          L[nL + i] = r;
+        }
+        nL += U1 - U0;  // read again only after the next epoch's first barrier
+      } else if (units) {
         __syncthreads();
         const ListRec* L = lists[cur];
         ListRec* L2 = lists[cur ^ 1];
