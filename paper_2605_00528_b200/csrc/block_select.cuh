@@ -23,6 +23,7 @@ struct BlockScratch {
   static constexpr int NW = BT / 32;
   static_assert((NW & (NW - 1)) == 0 && NW <= 32, "block size must be 32 x power of two");
   unsigned long long part[2][NW];
+  uint32_t part2[2][NW];  // second value of block_max2
   uint32_t hist[256];
   uint32_t sel_d, sel_above;
 };
@@ -41,6 +42,30 @@ __device__ __forceinline__ T block_reduce(T x, Op op, BlockScratch<BT>& sm, Par&
 #pragma unroll
   for (int o = NW / 2; o > 0; o >>= 1) y = op(y, __shfl_xor_sync(0xffffffffu, y, o));
   return y;
+}
+
+// two maxima (int64, uint32) in one collective (one barrier)
+template <int BT>
+__device__ __forceinline__ void block_max2(long long& x, uint32_t& y, BlockScratch<BT>& sm, Par& par) {
+  constexpr int NW = BT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
+  }
+  long long* bx = reinterpret_cast<long long*>(sm.part[par.p]);
+  uint32_t* by = sm.part2[par.p];
+  par.p ^= 1u;
+  if (lane == 0) { bx[wid] = x; by[wid] = y; }
+  __syncthreads();
+  x = bx[lane & (NW - 1)];
+  y = by[lane & (NW - 1)];
+#pragma unroll
+  for (int o = NW / 2; o > 0; o >>= 1) {
+    x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
+  }
 }
 
 // exclusive scan of one value per thread; *total receives the block sum

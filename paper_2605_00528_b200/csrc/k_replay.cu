@@ -770,8 +770,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
               tau = max(tau, (long long)(Te - r.t));
               smax = max(smax, owner_size(v, ck, ocall, r.lo));
             }
-            tau = block_reduce<RT, long long>(tau, Max(), sm.b, par);
-            smax = block_reduce<RT, uint32_t>(smax, Max(), sm.b, par);
+            block_max2<RT>(tau, smax, sm.b, par);  // eq:recency / eq:size normalisers, one barrier
             KeyCtx x;
             x.Te = Te; x.tau = tau; x.smax = smax;
             x.den = (int64_t)(a.p_high - a.p_low) * C;
