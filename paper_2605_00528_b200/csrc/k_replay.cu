@@ -154,6 +154,7 @@ struct ReplayArgs {
 struct Smem {
   BlockScratch<RT> b;
   uint32_t hist[H1];
+  uint32_t hist2[1024];  // second-level digit histogram (cleared with hist, no extra barrier)
   uint32_t res_j, res_rem, thr, item;
   uint32_t hb_j2, hb_j1;
   uint32_t n_app, n_piv, n_vict, n_vu, n_pu, pu_i;
@@ -770,6 +771,10 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
               tau = max(tau, (long long)(Te - r.t));
               smax = max(smax, owner_size(v, ck, ocall, r.lo));
             }
+            // both digit histograms are cleared here: the barrier of block_max2 orders the clear
+            // before pass b / b2 (their last readers were the previous epoch's find_level)
+            for (uint32_t i = threadIdx.x; i < H1; i += RT) sm.hist[i] = 0;
+            for (uint32_t i = threadIdx.x; i < 1024; i += RT) sm.hist2[i] = 0;
             block_max2<RT>(tau, smax, sm.b, par);  // eq:recency / eq:size normalisers, one barrier
             KeyCtx x;
             x.Te = Te; x.tau = tau; x.smax = smax;
@@ -779,8 +784,6 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
             const uint32_t act = nd.ev_act[j];
             PH(2);
             // pass b: per-unit key part kp = (!prot << 31) | q, weighted histogram of the top digit
-            for (uint32_t i = threadIdx.x; i < H1; i += RT) sm.hist[i] = 0;
-            __syncthreads();
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
               const ListRec r = L[i];
               const uint32_t c = cnt[r.u];
@@ -796,20 +799,18 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
             __syncthreads();
             uint32_t d1, r1, d2, r2;
             find_level<H1 / RT>(sm.hist, 0, H1, k, d1, r1, sm, par);
-            for (uint32_t i = threadIdx.x; i < 1024; i += RT) sm.hist[i] = 0;
-            __syncthreads();
             for (uint32_t i = threadIdx.x; i < nL; i += RT) {
               const uint32_t kp = L[i].kp;
               if (kp_digit(kp) != d1) continue;
               const uint32_t c = cnt[L[i].u];
-              if (c) atomicAdd(&sm.hist[kp & 1023u], c);
+              if (c) atomicAdd(&sm.hist2[kp & 1023u], c);
             }
             __syncthreads();
-            find_level<1024 / RT>(sm.hist, 0, 1024, r1, d2, r2, sm, par);
+            find_level<1024 / RT>(sm.hist2, 0, 1024, r1, d2, r2, sm, par);
             const uint32_t pb1 = d1 >= 1025u ? 1u : 0u;
             const uint32_t kps = (pb1 << 31) | ((d1 - pb1 * 1025u) << 10) | d2;
             const bool prot_piv = !(kps >> 31);
-            const bool whole = sm.hist[d2] == r2;  // the pivot units are evicted whole
+            const bool whole = sm.hist2[d2] == r2;  // the pivot units are evicted whole
             if (threadIdx.x == 0) { sm.n_piv = 0; sm.n_vu = 0; sm.n_pu = 0; }
             __syncthreads();
             PH(3);
