@@ -4,7 +4,7 @@ Holds no arithmetic of the method itself (see tracegen.py docstring)."""
 from .tracegen import (TraceDesc, make, make_c1, make_c2, make_c3, make_c4, make_c5, make_obs1,
                        make_chain_limit, make_random_small, make_stream_trace, default_place_cfg, default_replay_cfg,
                        PHYSICAL_CAP, N_SWEEP, CONFIGS, PLACE_KAPPA, place_cfg_for,
-                       TOOL_LABELS, pattern_labels, pattern_roles, make_label_markov)
+                       TOOL_LABELS, pattern_labels, pattern_roles, make_label_markov, make_hand_trace)
 import math
 
 

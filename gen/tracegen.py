@@ -813,3 +813,54 @@ def make_stream_trace(seq, epochs=None, n_nodes: int = 1, n_shared: int = 0) -> 
         session_block_lo=np.array([n_shared], np.uint32),
         session_block_len=np.array([max(nb - n_shared, 0)], np.uint32),
         type_shared_lo=np.array([0], np.uint32), type_shared_len=np.array([n_shared], np.uint32), **aeg)
+
+
+def make_hand_trace(calls, nodes, n_nodes: int = 1, shared=None, session_types=None) -> TraceDesc:
+    """A hand-written trace for pins whose expected result is derived by hand.
+
+    calls: list of dicts (t, s, v, prompt, out, new=prompt, last=0, blocks=[(lo, len), ...]), any
+           order (sorted here by (t, s)); block ids are global.
+    nodes: AEG nodes, list of dicts (ttl, obs, term=0, edges=[(dst, p, q16=65536), ...]).
+    shared: per agent type (lo, len) shared-prefix span (default: one type without a prefix).
+    Each session's private span is the hull of its blocks outside the shared spans."""
+    calls = sorted(calls, key=lambda c: (c["t"], c["s"]))
+    shared = shared or [(0, 0)]
+    ns = max(c["s"] for c in calls) + 1
+    styp = np.array(session_types if session_types is not None else [0] * ns, np.uint16)
+    b = _AEGBuilder()
+    for nd in nodes:
+        b.add_node(nd["ttl"], nd.get("obs", 0), bool(nd.get("term", 0)))
+    for u, nd in enumerate(nodes):
+        for e in nd.get("edges", []):
+            b.add_edge(u, e[0], e[1], e[2] if len(e) > 2 else 65536)
+    aeg = b.finish()
+    in_shared = lambda x: any(lo <= x < lo + ln for lo, ln in shared)
+    lo_s = [None] * ns
+    hi_s = [None] * ns
+    off, rlo, rln = [0], [], []
+    for c in calls:
+        for lo, ln in c["blocks"]:
+            rlo.append(lo); rln.append(ln)
+            for x in (lo, lo + ln - 1):
+                if not in_shared(x):
+                    s = c["s"]
+                    lo_s[s] = x if lo_s[s] is None else min(lo_s[s], x)
+                    hi_s[s] = x if hi_s[s] is None else max(hi_s[s], x)
+        off.append(len(rlo))
+    nb = max([lo + ln for lo, ln in zip(rlo, rln)] + [lo + ln for lo, ln in shared] + [1])
+    slo = np.array([0 if lo_s[s] is None else lo_s[s] for s in range(ns)], np.uint32)
+    sln = np.array([0 if lo_s[s] is None else hi_s[s] - lo_s[s] + 1 for s in range(ns)], np.uint32)
+    n = len(calls)
+    return TraceDesc(
+        name="hand", n_nodes=n_nodes, n_blocks=int(nb), seed=0,
+        call_t_us=np.array([c["t"] for c in calls], np.int64),
+        call_session=np.array([c["s"] for c in calls], np.uint32),
+        call_aeg_node=np.array([c["v"] for c in calls], np.uint32),
+        call_prompt_tokens=np.array([c["prompt"] for c in calls], np.uint32),
+        call_output_tokens=np.array([c["out"] for c in calls], np.uint32),
+        call_new_tokens=np.array([c.get("new", c["prompt"]) for c in calls], np.uint32),
+        call_is_last=np.array([c.get("last", 0) for c in calls], np.uint8),
+        call_range_off=np.array(off, np.uint32), range_block_lo=np.array(rlo, np.uint32),
+        range_len=np.array(rln, np.uint32), session_type=styp, session_block_lo=slo, session_block_len=sln,
+        type_shared_lo=np.array([lo for lo, _ in shared], np.uint32),
+        type_shared_len=np.array([ln for _, ln in shared], np.uint32), **aeg)

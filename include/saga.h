@@ -61,25 +61,29 @@ typedef enum {
                                 shared-prefix blocks only when no private candidate is left */
 } saga_policy;
 
-/* Counter slots, int64 each, 16 per (policy, capacity, node) replay (DESIGN.md §5 "Counters").
- * Identity: ACCESSES = HITS + MISSES + MIG_HITS + MIG_MISSES. */
+/* Counter slots, int64 each, 16 per (policy, capacity, node) replay: SURVEY §8.C.7's list, its
+ * reserved slot holding the peak resident count.  Identity: ACCESSES = HITS + MISSES + MIG_HITS +
+ * MIG_MISSES.  Unavoidable vs regenerated prefill follows P:881 ("tokens prefilled") and
+ * Observation 1: a CALL miss is compulsory only at the block's first touch in the
+ * whole trace (first call in (t, s) order touching it); every other CALL miss -- including the
+ * re-prefill of a rerouted session at its new node -- is regeneration. */
 enum {
   SAGA_C_ACCESSES = 0,
-  SAGA_C_HITS = 1,            /* CALL records found resident                                  */
-  SAGA_C_MISSES = 2,          /* CALL records not resident (tokens prefilled)          */
-  SAGA_C_MIG_HITS = 3,        /* MIG (migrated-in) records found resident                     */
-  SAGA_C_MIG_MISSES = 4,
-  SAGA_C_COMPULSORY = 5,      /* misses at the node's first touch of a block                  */
-  SAGA_C_INVALIDATED = 6,     /* residents dropped because their session migrated away (R1)   */
-  SAGA_C_EVICTIONS = 7,
-  SAGA_C_EVICT_PROTECTED = 8, /* AEG victims that were TTL-protected (hard pressure)   */
-  SAGA_C_EVICT_EVENTS = 9,
-  SAGA_C_REGEN_TOKENS = 10,   /* block_tokens x non-compulsory CALL misses                    */
-  SAGA_C_REGEN_US = 11,       /* their prefill time at prefill_tok_s                          */
-  SAGA_C_VICTIM_HASH = 12,    /* sum over victims of splitmix64((epoch << 32) | local id)     */
-  SAGA_C_INFEASIBLE_EPOCH = 13, /* first epoch whose requests exceed the capacity, else 0     */
-  SAGA_C_PEAK_RESIDENT = 14,
-  SAGA_C_EVENT_EPOCHS = 15,   /* epochs with records processed                                */
+  SAGA_C_HITS = 1,              /* CALL records found resident                                  */
+  SAGA_C_MISSES = 2,            /* CALL records not resident (tokens prefilled)          */
+  SAGA_C_COMPULSORY_GLOBAL = 3, /* CALL misses at the block's first touch in the whole trace    */
+  SAGA_C_COMPULSORY_NODE = 4,   /* misses (CALL or MIG) at the node's first touch of the block  */
+  SAGA_C_MIG_HITS = 5,          /* MIG (migrated-in) records found resident                     */
+  SAGA_C_MIG_MISSES = 6,
+  SAGA_C_INVALIDATED = 7,       /* residents dropped because their session migrated away (R1)   */
+  SAGA_C_EVICTIONS = 8,
+  SAGA_C_EVICT_PROTECTED = 9,   /* AEG victims that were TTL-protected (hard pressure)   */
+  SAGA_C_EVICT_EVENTS = 10,
+  SAGA_C_REGEN_TOKENS = 11,     /* block_tokens x (MISSES - COMPULSORY_GLOBAL)                  */
+  SAGA_C_REGEN_US = 12,         /* their prefill time at prefill_tok_s                          */
+  SAGA_C_VICTIM_HASH = 13,      /* sum over victims of splitmix64((epoch << 32) | local id)     */
+  SAGA_C_INFEASIBLE_EPOCH = 14, /* first epoch whose requests exceed the capacity, else 0       */
+  SAGA_C_PEAK_RESIDENT = 15,    /* max |S| after an epoch (<= capacity)                         */
   SAGA_NCOUNT = 16
 };
 

@@ -19,9 +19,9 @@ LIB = os.path.join(HERE, "libsaga_oracle.so")
 
 POL_AEG, POL_BELADY, POL_EVICT_ALL, POL_LRU, POL_LRU_PREFIX = 1, 2, 4, 8, 16
 INF = 0xFFFFFFFF
-COUNTERS = ["ACCESSES", "HITS", "MISSES", "MIG_HITS", "MIG_MISSES", "COMPULSORY", "INVALIDATED", "EVICTIONS",
-            "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH", "INFEASIBLE_EPOCH",
-            "PEAK_RESIDENT", "EVENT_EPOCHS"]
+COUNTERS = ["ACCESSES", "HITS", "MISSES", "COMPULSORY_GLOBAL", "COMPULSORY_NODE", "MIG_HITS", "MIG_MISSES",
+            "INVALIDATED", "EVICTIONS", "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH",
+            "INFEASIBLE_EPOCH", "PEAK_RESIDENT"]
 CI = {n: i for i, n in enumerate(COUNTERS)}
 
 _lock = threading.Lock()
@@ -29,7 +29,11 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle (g++ -O2 -ffp-contract=off, no -ffast-math, no SIMD intrinsics)."""
+    """Compile the oracle (g++ -O2 -ffp-contract=off, no -ffast-math, no SIMD intrinsics).
+
+    SAGA_ORACLE_LIB names a prebuilt library instead (scripts/mutate_oracle.py loads mutants)."""
+    if os.environ.get("SAGA_ORACLE_LIB"):
+        return os.environ["SAGA_ORACLE_LIB"]
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
                                "-o", LIB, SRC, "-lpthread"])
@@ -68,6 +72,8 @@ def lib():
             vp = C.c_void_p
             L.oracle_new.restype = vp
             L.oracle_new.argtypes = [C.POINTER(ODesc), C.POINTER(OPlace), C.POINTER(C.c_int)]
+            L.oracle_new_nodes.restype = vp
+            L.oracle_new_nodes.argtypes = [C.POINTER(ODesc), C.POINTER(OPlace), C.c_uint32, C.POINTER(C.c_int)]
             L.oracle_free.argtypes = [vp]
             L.oracle_placement.argtypes = [vp, vp, vp]
             L.oracle_migrations.argtypes = [vp, vp]
@@ -93,8 +99,9 @@ def lib():
             L.oracle_min_misses.argtypes = [vp, C.c_uint32, C.c_uint32]
             L.oracle_keys.argtypes = [vp, C.POINTER(OReplay), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_uint32, vp, vp, vp, C.c_uint64, vp, vp, vp]
-            L.oracle_eviction_score32.restype = C.c_float
-            L.oracle_eviction_score32.argtypes = [C.c_float] * 6
+            L.oracle_score32.restype = C.c_float
+            L.oracle_score32.argtypes = [C.c_float] * 3 + [C.c_int64, C.c_int64, C.c_uint32, C.c_uint32, C.c_float,
+                                                            C.POINTER(C.c_uint32)]
             L.oracle_reuse32.restype = C.c_float
             L.oracle_reuse32.argtypes = [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32]
             L.oracle_ttl_protect.restype = C.c_int
@@ -118,7 +125,7 @@ def replay_cfg(policy=POL_AEG, alpha=0.3, beta=0.5, gamma=0.2, p_low_pm=700, p_h
 class Oracle:
     """Owns one oracle instance over a TraceDesc (validation, placement and expansion run at build)."""
 
-    def __init__(self, desc, place_cfg: dict):
+    def __init__(self, desc, place_cfg: dict, node_mask: int = 0):
         self.desc = desc
         self._keep = {}
         arrs = {}
@@ -132,7 +139,7 @@ class Oracle:
                    place_cfg["theta_pm"], place_cfg["rmax_pm"], place_cfg["t_idle_us"], place_cfg["seed"])
         self.place_cfg = dict(place_cfg)
         err = C.c_int(0)
-        self.h = lib().oracle_new(C.byref(d), C.byref(p), C.byref(err))
+        self.h = lib().oracle_new_nodes(C.byref(d), C.byref(p), node_mask, C.byref(err))
         self.err = err.value
         if not self.h:
             raise ValueError(f"oracle: invalid trace (code {self.err})")
@@ -255,9 +262,12 @@ def select_topk(keys: np.ndarray, k: int) -> np.ndarray:
     return idx[:k]
 
 
-# scalar helpers (SPEC worked examples)
-def eviction_score32(alpha, beta, gamma, R, P, S):
-    return lib().oracle_eviction_score32(alpha, beta, gamma, R, P, S)
+# scalar entry points (SPEC worked examples): thin callers of the oracle's score() / reuse() / prot()
+def score32(alpha, beta, gamma, d, tau, size, smax, P):
+    """eq:eviction of a private unfinished candidate idle d of tau_max, size of size_max: (fp32, q)."""
+    q = C.c_uint32(0)
+    s = lib().oracle_score32(alpha, beta, gamma, d, tau, size, smax, P, C.byref(q))
+    return s, q.value
 
 
 def reuse32(p, q16, ncur, nobs):

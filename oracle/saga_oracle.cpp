@@ -84,10 +84,11 @@ namespace {
 const uint32_t INF = 0xFFFFFFFFu;
 enum { POL_AEG = 1, POL_BELADY = 2, POL_EVICT_ALL = 4, POL_LRU = 8, POL_LRU_PREFIX = 16 };
 // counter slots
+// (SURVEY §8.C.7's list; its reserved slot holds the peak resident count)
 enum {
-  C_ACCESSES, C_HITS, C_MISSES, C_MIG_HITS, C_MIG_MISSES, C_COMPULSORY, C_INVALIDATED, C_EVICTIONS,
-  C_EVICT_PROTECTED, C_EVICT_EVENTS, C_REGEN_TOKENS, C_REGEN_US, C_VICTIM_HASH, C_INFEASIBLE_EPOCH,
-  C_PEAK_RESIDENT, C_EVENT_EPOCHS, C_N
+  C_ACCESSES, C_HITS, C_MISSES, C_COMPULSORY_GLOBAL, C_COMPULSORY_NODE, C_MIG_HITS, C_MIG_MISSES,
+  C_INVALIDATED, C_EVICTIONS, C_EVICT_PROTECTED, C_EVICT_EVENTS, C_REGEN_TOKENS, C_REGEN_US, C_VICTIM_HASH,
+  C_INFEASIBLE_EPOCH, C_PEAK_RESIDENT, C_N
 };
 
 // public-domain splitmix64 finaliser (Steele/Lea/Flood; constants of SURVEY §8.C.2 P5)
@@ -144,6 +145,7 @@ struct Oracle {
   OPlace pc;
   // ---- derived ----
   std::vector<uint32_t> owner;        // owner[b]: session id, or n_sessions + type for shared prefix
+  std::vector<uint32_t> first_call;   // first call (global (t, s) order) whose ranges touch block b
   std::vector<uint32_t> ecall;        // admission epoch e(c) = floor(t_c / E) + 1
   std::vector<std::vector<uint32_t>> scalls;  // calls of each session in order
   std::vector<uint8_t> node_of;
@@ -152,6 +154,7 @@ struct Oracle {
   int64_t n_steals = 0, n_reroutes = 0;
   std::map<std::pair<uint32_t, uint32_t>, uint32_t> act_log;  // (e, w) -> mask
   std::vector<NodeData> nodes;
+  uint32_t node_mask = 0;             // nodes whose streams expand() builds (0 = all)
   int err = 0;
 
   int validate() {
@@ -240,11 +243,6 @@ struct Oracle {
       for (auto& q : Q[w]) L += std::min(q.rem, E);
       return L;
     };
-    auto active = [&](uint32_t w) {
-      int64_t a = 0;
-      for (uint32_t x = 0; x < n_types; ++x) a += cnt[w][x];
-      return a;
-    };
     for (uint64_t e = 1;; ++e) {
       bool any = false;
       for (uint32_t w = 0; w < W; ++w) any |= !Q[w].empty();
@@ -303,12 +301,10 @@ struct Oracle {
         uint32_t w;
         if (cached && 1000 * load(uint32_t(ws)) < int64_t(pc.theta_pm) * K * E) {
           w = uint32_t(ws);
-        } else {  // argmin load, ties -> fewer active sessions -> lower node id
+        } else {  // argmin load, ties -> lowest worker id
           w = 0;
-          for (uint32_t x = 1; x < W; ++x) {
-            int64_t lx = load(x), lw = load(w);
-            if (lx < lw || (lx == lw && active(x) < active(w))) w = x;
-          }
+          for (uint32_t x = 1; x < W; ++x)
+            if (load(x) < load(w)) w = x;
         }
         int64_t pf = (cached && int32_t(w) == ws) ? newt[c] : prompt[c];
         int64_t omega = ceil_div(pf * 1000000, pc.prefill_tok_s) + ceil_div(int64_t(outt[c]) * 1000000, pc.decode_tok_s);
@@ -378,6 +374,7 @@ struct Oracle {
     }
     for (uint32_t w = 0; w < n_nodes; ++w) {
       NodeData& nd = nodes[w];
+      if (node_mask && !((node_mask >> w) & 1u)) continue;   // stream not requested (left empty)
       for (auto& kv : evs[w]) {
         Event x = kv.second;
         std::sort(x.inv.begin(), x.inv.end());
@@ -497,21 +494,41 @@ struct Oracle {
     st.ttl_base = ttl_of(uint32_t(c));
     float P = 0.0f;
     double P64 = 0.0;
-    if (!st.fin) {
-      for (uint32_t k = eoff[v]; k < eoff[v + 1]; ++k) {              // eq:reuse: sum_u P(v->u) overlap(s,u)
-        uint64_t nsh = (ncur * uint64_t(eq16[k])) >> 16;             // per-branch shared prefix
-        uint64_t den = ncur + obs_of(uint32_t(c));
-        float ov = den == 0 ? 1.0f : float(int64_t(nsh)) / float(int64_t(den));   // n_cur/(n_cur+n_obs)
-        double ov64 = den == 0 ? 1.0 : double(nsh) / double(den);
-        P = P + ep[k] * ov;
-        P64 = P64 + double(ep[k]) * ov64;
-      }
-      P = std::fmin(P, 1.0f);
-      P64 = std::fmin(P64, 1.0);
-    }
+    if (!st.fin)
+      P = reuse(&ep[eoff[v]], &eq16[eoff[v]], eoff[v + 1] - eoff[v], ncur, obs_of(uint32_t(c)), &P64);
     st.P = P;
     st.P64 = P64;
     return st;
+  }
+
+  // eq:reuse  P_reuse(s) = sum_u P(v->u) * overlap(s, u) over the out-edges of v in
+  // CSR order, with eq:overlap's linear form n_sh / (n_cur + n_obs) per edge (DESIGN.md
+  // R-overlap), clamped to 1 (R-clamp); fp32 in this order, plus the fp64 value
+  static float reuse(const float* p, const uint32_t* q16, uint32_t n_edges, uint64_t ncur, uint64_t nobs, double* P64) {
+    float P = 0.0f;
+    double D = 0.0;
+    for (uint32_t k = 0; k < n_edges; ++k) {
+      uint64_t nsh = (ncur * uint64_t(q16[k])) >> 16;              // per-branch shared prefix
+      uint64_t den = ncur + nobs;
+      float ov = den == 0 ? 1.0f : float(int64_t(nsh)) / float(int64_t(den));   // n_cur/(n_cur+n_obs)
+      double ov64 = den == 0 ? 1.0 : double(nsh) / double(den);
+      P = P + p[k] * ov;
+      D = D + double(p[k]) * ov64;
+    }
+    if (P64) *P64 = std::fmin(D, 1.0);
+    return std::fmin(P, 1.0f);
+  }
+
+  // per-event context of the key: T_e, and the exact-integer memory pressure m = num / den of
+  // eq:pressure at occupancy occ = |S| after R1 and capacity C; the normalisers
+  // tau_max / size_max start at 0 / 1 and are maxed over the candidates by the caller (R-norm)
+  static Ctx make_ctx(const OReplay& cfg, uint32_t e, int64_t Te, int64_t occ, uint32_t C, uint32_t act) {
+    Ctx x{};
+    x.e = e; x.Te = Te; x.tau = 0; x.smax = 1;
+    x.den = int64_t(cfg.p_high_pm - cfg.p_low_pm) * C;
+    x.num = std::min<int64_t>(x.den, std::max<int64_t>(0, 1000 * occ - int64_t(cfg.p_low_pm) * C));
+    x.act = act;
+    return x;
   }
 
   static void score(const OReplay& cfg, const Ctx& x, const OwnerState& st, const KeyIn& b,
@@ -537,7 +554,9 @@ struct Oracle {
     if (st.fin) return false;
     int64_t el = x.Te - st.t_call;
     if (!(el < cfg.ttl_max_us)) return false;
-    return 2 * x.den * el < st.ttl_base * (2 * x.den - x.num);
+    // el < ttl_base * (1 - m/2) with m = num/den, multiplied out (128-bit: no overflow for any
+    // capacity / ttl the ABI accepts)
+    return (__int128)2 * x.den * el < (__int128)st.ttl_base * (2 * x.den - x.num);
   }
 
   // ------------------------------------------------------------------------------------------
@@ -581,11 +600,7 @@ struct Oracle {
         for (uint32_t b : S) if (!A.count(b)) cand.push_back(b);
         std::vector<std::pair<uint64_t, uint32_t>> keys;  // (key, lid)
         if (cfg.policy == POL_AEG) {
-          Ctx x{};
-          x.e = e; x.Te = Te; x.tau = 0; x.smax = 1;
-          x.den = int64_t(cfg.p_high_pm - cfg.p_low_pm) * C;
-          x.num = std::min<int64_t>(x.den, std::max<int64_t>(0, 1000 * int64_t(S.size()) - int64_t(cfg.p_low_pm) * C));
-          x.act = ev.act;
+          Ctx x = make_ctx(cfg, e, Te, int64_t(S.size()), C, ev.act);
           std::vector<OwnerState> sts;
           for (uint32_t b : cand) {
             x.tau = std::max(x.tau, Te - tl[b]);                       // tau_max over candidates
@@ -641,18 +656,20 @@ struct Oracle {
             res[b] = 1; S.insert(b);
             if (g.kind == 0) {
               ctr[C_MISSES]++;
-              if (!nd.ftn[p]) { ctr[C_REGEN_TOKENS] += btok; ctr[C_REGEN_US] += int64_t(btok) * 1000000 / pc.prefill_tok_s; }
+              // "tokens prefilled": a CALL miss is unavoidable only at the block's first
+              // touch in the whole trace; a re-prefill elsewhere (reroute) is regeneration
+              if (first_call[nd.block[p]] == g.call) ctr[C_COMPULSORY_GLOBAL]++;
+              else { ctr[C_REGEN_TOKENS] += btok; ctr[C_REGEN_US] += int64_t(btok) * 1000000 / pc.prefill_tok_s; }
             } else {
               ctr[C_MIG_MISSES]++;
             }
-            if (nd.ftn[p]) ctr[C_COMPULSORY]++;
+            if (nd.ftn[p]) ctr[C_COMPULSORY_NODE]++;
           }
           tl[b] = g.tval;
           nu[b] = nd.next_use[p];
           lp[b] = uint32_t(p);
         }
       ctr[C_PEAK_RESIDENT] = std::max<int64_t>(ctr[C_PEAK_RESIDENT], int64_t(S.size()));
-      ctr[C_EVENT_EPOCHS]++;
     }
     ctr[C_VICTIM_HASH] = int64_t(hash);
   }
@@ -684,8 +701,9 @@ struct Oracle {
   }
 };
 
-Oracle* build(const ODesc* d, const OPlace* p, int* err) {
+Oracle* build(const ODesc* d, const OPlace* p, uint32_t node_mask, int* err) {
   Oracle* o = new Oracle();
+  o->node_mask = node_mask;
   o->n_calls = d->n_calls; o->n_sessions = d->n_sessions; o->n_types = d->n_types; o->n_aeg = d->n_aeg_nodes;
   o->n_edges = d->n_edges; o->n_ranges = d->n_ranges; o->n_blocks = d->n_blocks; o->n_nodes = d->n_nodes;
   o->btok = d->block_tokens;
@@ -711,6 +729,13 @@ Oracle* build(const ODesc* d, const OPlace* p, int* err) {
     for (uint32_t i = 0; i < o->tlen[a]; ++i) o->owner[o->tlo[a] + i] = o->n_sessions + a;
   for (uint32_t s = 0; s < o->n_sessions; ++s)
     for (uint32_t i = 0; i < o->slen[s]; ++i) o->owner[o->slo[s] + i] = s;
+  // first_touch_global: walk the calls in (t, s) order; a block's first toucher
+  // is the call that finds it untouched
+  o->first_call.assign(o->n_blocks, 0xFFFFFFFFu);
+  for (uint32_t c = 0; c < o->n_calls; ++c)
+    for (uint32_t r = o->roff[c]; r < o->roff[c + 1]; ++r)
+      for (uint32_t i = 0; i < o->rlen[r]; ++i)
+        if (o->first_call[o->rlo[r] + i] == 0xFFFFFFFFu) o->first_call[o->rlo[r] + i] = c;
   o->ecall.resize(o->n_calls);
   o->scalls.assign(o->n_sessions, {});
   for (uint32_t c = 0; c < o->n_calls; ++c) {
@@ -730,7 +755,9 @@ Oracle* build(const ODesc* d, const OPlace* p, int* err) {
 // ============================================================================================
 extern "C" {
 
-void* oracle_new(const ODesc* d, const OPlace* p, int* err) { return build(d, p, err); }
+void* oracle_new(const ODesc* d, const OPlace* p, int* err) { return build(d, p, 0, err); }
+// as oracle_new, but only the streams of the nodes in node_mask are expanded (large traces)
+void* oracle_new_nodes(const ODesc* d, const OPlace* p, uint32_t node_mask, int* err) { return build(d, p, node_mask, err); }
 void oracle_free(void* h) { delete static_cast<Oracle*>(h); }
 
 void oracle_placement(void* h, uint8_t* node_out, int64_t* stats /*[steals, reroutes, n_mig]*/) {
@@ -871,11 +898,7 @@ void oracle_keys(void* h, const OReplay* cfg, uint32_t w, uint32_t e, uint32_t o
     for (uint64_t i = 0; i < n; ++i) key[i] = (uint64_t(nu[i]) << 32) | lid[i];
     return;
   }
-  Oracle::Ctx x{};
-  x.e = e; x.Te = int64_t(e) * o->pc.epoch_us; x.tau = 0; x.smax = 1;
-  x.den = int64_t(cfg->p_high_pm - cfg->p_low_pm) * cap;
-  x.num = std::min<int64_t>(x.den, std::max<int64_t>(0, 1000 * int64_t(occ) - int64_t(cfg->p_low_pm) * cap));
-  x.act = act;
+  Oracle::Ctx x = Oracle::make_ctx(*cfg, e, int64_t(e) * o->pc.epoch_us, int64_t(occ), cap, act);
   std::vector<Oracle::OwnerState> sts(n);
   for (uint64_t i = 0; i < n; ++i) {
     x.tau = std::max(x.tau, x.Te - t_last[i]);
@@ -893,28 +916,38 @@ void oracle_keys(void* h, const OReplay* cfg, uint32_t w, uint32_t e, uint32_t o
   }
 }
 
-// Scalar helpers used by the pins of SPEC's worked examples (eq:eviction, eq:reuse, eq:overlap,
-// Alg. alg:ttl, eq:pressure) -- same arithmetic as score()/owner_state()/prot() above.
-float oracle_eviction_score32(float alpha, float beta, float gamma, float R, float P, float S) {
-  return ((alpha * R) + (beta * (1.0f - P))) + (gamma * S);
+// Scalar entry points for the pins of SPEC's worked examples.  Each one is a thin caller of the
+// function replay() uses: score() (eq:eviction / eq:recency / eq:size), reuse() (eq:reuse +
+// eq:overlap) and prot() with make_ctx() (Alg. alg:ttl + eq:pressure).
+// score of a private, unfinished candidate: idle d of tau_max, size of size_max, P_reuse P
+float oracle_score32(float alpha, float beta, float gamma, int64_t d, int64_t tau, uint32_t size, uint32_t smax,
+                     float P, uint32_t* q) {
+  OReplay cfg{POL_AEG, alpha, beta, gamma, 700, 900, 300000000};
+  Oracle::Ctx x = Oracle::make_ctx(cfg, 1, d, 0, 1, 0);   // T_e = d with t_last = 0
+  x.tau = tau;
+  x.smax = smax;
+  Oracle::OwnerState st{};
+  st.size = size;
+  st.P = P;
+  st.P64 = P;
+  Oracle::KeyIn b{0, 0, 0};
+  float s32; double s64; uint32_t qq;
+  Oracle::score(cfg, x, st, b, &s32, &s64, &qq);
+  if (q) *q = qq;
+  return s32;
 }
 float oracle_reuse32(const float* p, const uint32_t* q16, uint32_t n_edges, uint32_t ncur, uint32_t nobs) {
-  float P = 0.0f;
-  for (uint32_t k = 0; k < n_edges; ++k) {
-    uint64_t nsh = (uint64_t(ncur) * q16[k]) >> 16;
-    uint64_t den = uint64_t(ncur) + nobs;
-    float ov = den == 0 ? 1.0f : float(int64_t(nsh)) / float(int64_t(den));
-    P = P + p[k] * ov;
-  }
-  return std::fmin(P, 1.0f);
+  return Oracle::reuse(p, q16, n_edges, ncur, nobs, nullptr);
 }
-// protected?  el = T_e - t_call; returns 1 if the TTL (scaled by 1 - m/2) still covers el
+// protected?  el = T_e - t_call (a private, unfinished owner); 1 if the TTL (scaled by 1 - m/2) covers el
 int oracle_ttl_protect(int64_t el, int64_t ttl_base, int64_t ttl_max, uint32_t occ, uint32_t cap,
                        uint32_t low_pm, uint32_t high_pm) {
-  int64_t den = int64_t(high_pm - low_pm) * cap;
-  int64_t num = std::min<int64_t>(den, std::max<int64_t>(0, 1000 * int64_t(occ) - int64_t(low_pm) * cap));
-  if (!(el < ttl_max)) return 0;
-  return 2 * den * el < ttl_base * (2 * den - num) ? 1 : 0;
+  OReplay cfg{POL_AEG, 0.3f, 0.5f, 0.2f, low_pm, high_pm, ttl_max};
+  Oracle::Ctx x = Oracle::make_ctx(cfg, 1, el, int64_t(occ), cap, 0);   // t_call = 0
+  Oracle::OwnerState st{};
+  st.t_call = 0;
+  st.ttl_base = ttl_base;
+  return Oracle::prot(cfg, x, st) ? 1 : 0;
 }
 uint64_t oracle_splitmix64(uint64_t x) { return splitmix64(x); }
 }

@@ -125,15 +125,21 @@ __global__ void k_ev_finish(uint32_t J, uint32_t G, uint32_t w, uint32_t* ev_e, 
 }
 
 // one warp per group: write the global block ids of the group's ranges at its positions
-__global__ void k_fill_stream(TraceView v, const uint32_t* g_call, const uint64_t* g_pos, uint32_t G, uint32_t* block) {
+// and mark the CALL records that are their block's first touch in the whole trace (ftg bitmap)
+__global__ void k_fill_stream(TraceView v, const uint32_t* g_call, const uint32_t* g_kind, const uint64_t* g_pos,
+                              uint32_t G, uint32_t* block, uint32_t* ftg) {
   const int lane = threadIdx.x & 31;
   for (uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < G; g += (gridDim.x * blockDim.x) >> 5) {
     const uint32_t c = g_call[g];
     if (c == NONE) continue;
+    const bool call_rec = g_kind[g] == 0;
     uint64_t p = g_pos[g];
     for (uint32_t r = v.roff[c]; r < v.roff[c + 1]; ++r) {
       const uint32_t lo = v.rlo[r], n = v.rlen[r];
-      for (uint32_t i = lane; i < n; i += 32) block[p + i] = lo + i;
+      for (uint32_t i = lane; i < n; i += 32) {
+        block[p + i] = lo + i;
+        if (call_rec && v.fcall[lo + i] == c) atomicOr(&ftg[(p + i) >> 5], 1u << ((p + i) & 31));
+      }
       p += n;
     }
   }
@@ -216,7 +222,8 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
   nd.inv_s = dalloc<uint32_t>(t, nI);
   nd.inv_e = dalloc<uint32_t>(t, nI);
   nd.block = dalloc<uint32_t>(t, N);
-  if (!nd.ev_e || !nd.ev_g || !nd.ev_inv || !nd.ev_act || !nd.inv_s || !nd.inv_e || !nd.block) {
+  nd.ftg = dalloc<uint32_t>(t, N / 32 + 1);
+  if (!nd.ev_e || !nd.ev_g || !nd.ev_inv || !nd.ev_act || !nd.inv_s || !nd.inv_e || !nd.block || !nd.ftg) {
     set_error("out of device memory (expand)");
     return SAGA_ERR_OOM;
   }
@@ -228,8 +235,9 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
                                                                   nd.inv_s, nd.inv_e, nd.ev_inv, t->act, t->n_act,
                                                                   nd.ev_act);
   count_launch();
+  SAGA_CK(cudaMemsetAsync(nd.ftg, 0, (N / 32 + 1) * 4, s));
   if (G > 0) {
-    k_fill_stream<<<grid_for(uint64_t(G) * 32), NTHREADS, 0, s>>>(v, nd.g_call, nd.g_pos, G, nd.block);
+    k_fill_stream<<<grid_for(uint64_t(G) * 32), NTHREADS, 0, s>>>(v, nd.g_call, nd.g_kind, nd.g_pos, G, nd.block, nd.ftg);
     count_launch();
   }
   SAGA_CK_LAUNCH();

@@ -126,6 +126,17 @@ __global__ void k_call_derived(TraceView v, uint32_t* ecall, int64_t* tend, uint
   }
 }
 
+// first_touch_global: the smallest call index (= earliest in (t, s) order) whose ranges touch the
+// block; one warp per call, one atomicMin per accessed block (deterministic)
+__global__ void k_first_call(TraceView v, uint32_t* fcall) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < v.n_calls; c += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t r = v.roff[c]; r < v.roff[c + 1]; ++r) {
+      const uint32_t lo = v.rlo[r], n = v.rlen[r];
+      for (uint32_t i = lane; i < n; i += 32) atomicMin(&fcall[lo + i], c);
+    }
+}
+
 __global__ void k_sess_scatter(TraceView v, const uint32_t* sc_off, uint32_t* fill, uint32_t* sc_call) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < v.n_calls; c += gridDim.x * blockDim.x) {
     uint32_t s = v.call_sess[c];
@@ -242,6 +253,14 @@ saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d) {
     return SAGA_ERR_TRACE;
   }
   v.owner = owner;
+  uint32_t* fcall = dalloc<uint32_t>(t, d->n_blocks);
+  if (!fcall) { set_error("saga_load_trace: out of device memory"); return SAGA_ERR_OOM; }
+  SAGA_CK(cudaMemsetAsync(fcall, 0xFF, size_t(d->n_blocks) * 4, t->stream));
+  if (d->n_calls) {
+    k_first_call<<<grid_for(uint64_t(d->n_calls) * 32), NTHREADS, 0, t->stream>>>(v, fcall);
+    count_launch();
+  }
+  v.fcall = fcall;
   // derived per-call tables
   uint32_t* ecall = dalloc<uint32_t>(t, d->n_calls);
   int64_t* tend = dalloc<int64_t>(t, d->n_calls);

@@ -126,7 +126,8 @@ __global__ void k_ev_pos(const uint64_t* g_pos, const uint32_t* ev_g, uint32_t J
 }
 
 // stream order: NFIE marks, per-event distinct / first-touch / last-touch counts
-__global__ void __launch_bounds__(SS_T) k_epoch_stats(const uint32_t* __restrict__ nxt, uint32_t* lidf, uint64_t n,
+__global__ void __launch_bounds__(SS_T) k_epoch_stats(const uint32_t* __restrict__ nxt, uint32_t* lidf,
+                                                      const uint32_t* __restrict__ ftg, uint64_t n,
                                                       const uint64_t* __restrict__ ev_pos, uint32_t J,
                                                       uint32_t* cnt_dist, uint32_t* cnt_first, uint32_t* cnt_last) {
   __shared__ uint32_t s_j0;
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(SS_T) k_epoch_stats(const uint32_t* __restrict
     if ((uint64_t)q >= end) ++cd;                 // last record of its block in this epoch
     else atomicOr(&lidf[q], LID_NFIE);            // the block repeats later in the same epoch
     if (lidf[p] & LID_FTN) ++cf;
+    if ((ftg[p >> 5] >> (p & 31)) & 1u) atomicOr(&lidf[p], LID_FTG);   // global first touch (rare)
   }
   if (cd) atomicAdd(&cnt_dist[j], cd);
   if (cf) atomicAdd(&cnt_first[j], cf);
@@ -286,7 +288,7 @@ saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* nu_out, uint32_t* 
     k_ev_pos<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(nd.g_pos, nd.ev_g, J, ev_pos);
     count_launch();
     if (N > 0) {
-      k_epoch_stats<<<(unsigned)((N + SS_TILE - 1) / SS_TILE), SS_T, 0, s>>>(nd.nxt, nd.lidf, N, ev_pos, J, cd, cf, cl);
+      k_epoch_stats<<<(unsigned)((N + SS_TILE - 1) / SS_TILE), SS_T, 0, s>>>(nd.nxt, nd.lidf, nd.ftg, N, ev_pos, J, cd, cf, cl);
       count_launch();
     }
     k_sweep<<<1, SW_T, 0, s>>>(cd, cf, cl, Jr, sw);

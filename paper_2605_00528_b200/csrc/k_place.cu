@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   off += (size_t)W * Q * 4;
   uint32_t* wR = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * Q;   // W: work (us)
   __shared__ int32_t cnt[32][32];                       // sessions with aff = w, !fin, by type
-  __shared__ int32_t act_tot[32];
   // call records streamed ahead by TMA bulk copies: chunk j (calls [256 j, 256 j + 256)) lives
   // in buffer j & 1; chunk j + 1 is requested when chunk j is first touched
   constexpr uint32_t CH = 256;
@@ -112,7 +111,6 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   __shared__ uint32_t xfer_n, n_mig, n_act, errf;
   __shared__ unsigned long long steals, reroutes;
   for (int i = lane; i < 32 * 32; i += 32) (&cnt[0][0])[i] = 0;
-  act_tot[lane] = 0;
   if (SS) {
     const SessRec init{-1, 0u, 0ll};
     for (uint32_t i = lane; i < NS; i += 32) { sess[i] = init; moved[i] = 0; }
@@ -297,7 +295,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           const uint32_t ty = v.styp[s];
           if (!(sr.ttlf & S_FIN)) {  // s is counted at its current affinity node
             const int32_t ao = sr.aff;
-            cnt[ao][ty]--; act_tot[ao]--; cnt[th][ty]++; act_tot[th]++;
+            cnt[ao][ty]--; cnt[th][ty]++;
           }
           sr.aff = (int32_t)th;
           sess[s] = sr;
@@ -333,16 +331,14 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
         uint32_t w;
         if (cached && 1000 * Lws < (int64_t)a.theta_pm * (int64_t)K * E) {
           w = (uint32_t)ws;
-        } else {  // argmin load; ties -> fewer active sessions -> lowest id
+        } else {  // argmin load; ties -> lowest worker id
           int64_t kL = act_lane ? L : INT64_MAX;
-          int32_t kA = act_lane ? act_tot[lane] : INT32_MAX;
           uint32_t kW = lane;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             int64_t oL = __shfl_xor_sync(0xffffffffu, (long long)kL, o);
-            int32_t oA = __shfl_xor_sync(0xffffffffu, kA, o);
             uint32_t oW = __shfl_xor_sync(0xffffffffu, kW, o);
-            if (oL < kL || (oL == kL && (oA < kA || (oA == kA && oW < kW)))) { kL = oL; kA = oA; kW = oW; }
+            if (oL < kL || (oL == kL && oW < kW)) { kL = oL; kW = oW; }
           }
           w = kW;
         }
@@ -364,8 +360,8 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
         }
         if (lane == 0) {
           if (ws >= 0 && w != (uint32_t)ws) ++reroutes;
-          if (ws >= 0 && !fin_old) { cnt[ws][tyi]--; act_tot[ws]--; }
-          if (!f_new) { cnt[w][tyi]++; act_tot[w]++; }
+          if (ws >= 0 && !fin_old) cnt[ws][tyi]--;
+          if (!f_new) cnt[w][tyi]++;
         }
         if (lane == i) a.node_of[c] = (uint8_t)w;
         // forward the post-call state to later lanes of the same session in this batch

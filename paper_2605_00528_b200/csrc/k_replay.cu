@@ -550,8 +550,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
     uint32_t nL = 0;      // live unit list length (uniform)
     int cur = 0;          // active list buffer
     uint32_t ucur = 0;    // session-update cursor (uniform)
-    long long c_hit = 0, c_miss = 0, c_mhit = 0, c_mmiss = 0, c_comp = 0, c_regen = 0, c_inv = 0;
-    long long c_ev = 0, c_prot = 0, c_evev = 0, c_events = 0, c_peak = 0, infeasible = 0;
+    long long c_hit = 0, c_miss = 0, c_mhit = 0, c_mmiss = 0, c_comp = 0, c_compg = 0, c_regen = 0, c_inv = 0;
+    long long c_ev = 0, c_prot = 0, c_evev = 0, c_peak = 0, infeasible = 0;
     unsigned long long hash = 0;
     uint32_t bad = 0;
     long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_t = clock64();
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       PH(0);
       // ---- R2: |A|, new = |A \ S|; hits / misses; in-flight blocks leave the index ----
       uint32_t nA = 0, nnew = 0;
-      uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_comp = 0, t_regen = 0;
+      uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_comp = 0, t_compg = 0, t_regen = 0;
       // A first-in-epoch record p is a hit iff bit p of the next-use-resident bitmap is set (the
       // resident block's next use is p); a warp's 32 positions are one aligned bitmap word.
       uint32_t* nres = belady ? pend.bits : nres_a;
@@ -677,7 +677,9 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           if (in[u]) {
             if (first && !resident) {
               ++nA; ++nnew;
-              if (mig) ++t_mmiss; else { ++t_miss; if (!(lf[u] & LID_FTN)) ++t_regen; }
+              // CALL miss: compulsory only at the block's first touch in the whole trace, else a
+              // re-prefill = regeneration ("tokens prefilled"), also after a reroute
+              if (mig) ++t_mmiss; else { ++t_miss; if (lf[u] & LID_FTG) ++t_compg; else ++t_regen; }
               if (lf[u] & LID_FTN) ++t_comp;
             } else {
               if (first) ++nA;
@@ -705,7 +707,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
         nnew = (uint32_t)pk;
       }
       if (nA > C) { infeasible = e; break; }
-      c_hit += t_hit; c_miss += t_miss; c_mhit += t_mhit; c_mmiss += t_mmiss; c_comp += t_comp; c_regen += t_regen;
+      c_hit += t_hit; c_miss += t_miss; c_mhit += t_mhit; c_mmiss += t_mmiss; c_comp += t_comp; c_compg += t_compg;
+      c_regen += t_regen;
       const uint32_t inAS = nA - nnew;  // in-flight (resident) blocks
       const int64_t kk = (pol == SAGA_POLICY_EVICT_ALL) ? (int64_t)S - (int64_t)inAS
                                                         : (int64_t)S + (int64_t)nnew - (int64_t)C;
@@ -1032,7 +1035,6 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       }
       PH(7);
       c_peak = max(c_peak, (long long)S);
-      c_events += 1;
     }
     // ---- counters ----
     if (pf_j != NONE) await_pf();  // no bulk copy may target the staging area after the item
@@ -1043,7 +1045,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       atomicAdd(&sc[SAGA_C_MISSES], (unsigned long long)c_miss);
       atomicAdd(&sc[SAGA_C_MIG_HITS], (unsigned long long)c_mhit);
       atomicAdd(&sc[SAGA_C_MIG_MISSES], (unsigned long long)c_mmiss);
-      atomicAdd(&sc[SAGA_C_COMPULSORY], (unsigned long long)c_comp);
+      atomicAdd(&sc[SAGA_C_COMPULSORY_NODE], (unsigned long long)c_comp);
+      atomicAdd(&sc[SAGA_C_COMPULSORY_GLOBAL], (unsigned long long)c_compg);
       atomicAdd(&sc[SAGA_C_REGEN_TOKENS], (unsigned long long)c_regen);
       atomicAdd(&sc[SAGA_C_VICTIM_HASH], hash);
     }
@@ -1057,7 +1060,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       out[SAGA_C_MISSES] = s_ctr[SAGA_C_MISSES];
       out[SAGA_C_MIG_HITS] = s_ctr[SAGA_C_MIG_HITS];
       out[SAGA_C_MIG_MISSES] = s_ctr[SAGA_C_MIG_MISSES];
-      out[SAGA_C_COMPULSORY] = s_ctr[SAGA_C_COMPULSORY];
+      out[SAGA_C_COMPULSORY_GLOBAL] = s_ctr[SAGA_C_COMPULSORY_GLOBAL];
+      out[SAGA_C_COMPULSORY_NODE] = s_ctr[SAGA_C_COMPULSORY_NODE];
       out[SAGA_C_INVALIDATED] = c_inv;
       out[SAGA_C_EVICTIONS] = c_ev;
       out[SAGA_C_EVICT_PROTECTED] = c_prot;
@@ -1067,7 +1071,6 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       out[SAGA_C_VICTIM_HASH] = s_ctr[SAGA_C_VICTIM_HASH];
       out[SAGA_C_INFEASIBLE_EPOCH] = infeasible;
       out[SAGA_C_PEAK_RESIDENT] = c_peak;
-      out[SAGA_C_EVENT_EPOCHS] = c_events;
       if (a.item_cyc) a.item_cyc[it] = (unsigned long long)(clock64() - t_start);
       if (a.phase_cyc)
         for (int i = 0; i < 8; ++i) a.phase_cyc[(uint64_t)it * 8 + i] = (unsigned long long)ph[i];

@@ -18,7 +18,8 @@ constexpr uint32_t NONE = 0xFFFFFFFFu;
 // packed per-position word of a node stream after next-use: local id | flags
 constexpr uint32_t LID_FTN = 1u << 31;   // first touch of the block at this node
 constexpr uint32_t LID_NFIE = 1u << 30;  // NOT the first record of the block in its epoch
-constexpr uint32_t LID_MASK = (1u << 30) - 1;
+constexpr uint32_t LID_FTG = 1u << 29;   // CALL record that is the block's first touch in the whole trace
+constexpr uint32_t LID_MASK = (1u << 29) - 1;
 constexpr int NTHREADS = 256;
 
 extern std::atomic<uint64_t> g_launches;
@@ -89,6 +90,7 @@ struct TraceView {
   const int64_t* tend;     // tool start t_c + prefill(new) + decode(out)
   const uint64_t* rsum;    // blocks accessed by the call
   const uint32_t* owner;   // [n_blocks] session, or n_sessions + type, or NONE
+  const uint32_t* fcall;   // [n_blocks] first call (global (t, s) order) touching the block, or NONE
   const uint32_t* sc_off;  // [n_sessions+1] calls of each session (CSR, ascending)
   const uint32_t* sc_call;
   const float* ci_P;       // P_reuse(s) after call c (eq:reuse + eq:overlap), fp32 pinned
@@ -104,6 +106,7 @@ struct NodeDev {
   uint32_t G = 0;          // record groups
   uint32_t n_inv = 0;
   uint32_t* block = nullptr;
+  uint32_t* ftg = nullptr;     // [N/32+1] bit p: CALL record p is its block's global first touch
   uint64_t* g_pos = nullptr;   // [G+1]
   int64_t* g_t = nullptr;      // [G]
   uint32_t* g_call = nullptr;  // [G]
@@ -260,7 +263,8 @@ __device__ __forceinline__ bool ttl_protected(const KeyCtx& x, const OwnerKeyIn&
   if (o.fin) return false;
   int64_t el = x.Te - o.t_call;
   if (!(el < x.ttl_max)) return false;
-  return 2 * x.den * el < o.ttl_base * (2 * x.den - x.num);
+  // 128-bit products: exact for every capacity / TTL the ABI accepts
+  return (__int128)2 * x.den * el < (__int128)o.ttl_base * (2 * x.den - x.num);
 }
 
 __device__ __forceinline__ uint64_t aeg_key(bool prot, uint32_t q, uint32_t lid) {

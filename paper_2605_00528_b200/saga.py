@@ -16,9 +16,9 @@ LIB_PATH = os.path.join(PKG, "libsaga.so")
 
 POLICY_AEG, POLICY_BELADY, POLICY_EVICT_ALL, POLICY_LRU, POLICY_LRU_PREFIX = 1, 2, 4, 8, 16
 NCOUNT = 16
-COUNTERS = ["ACCESSES", "HITS", "MISSES", "MIG_HITS", "MIG_MISSES", "COMPULSORY", "INVALIDATED", "EVICTIONS",
-            "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH", "INFEASIBLE_EPOCH",
-            "PEAK_RESIDENT", "EVENT_EPOCHS"]
+COUNTERS = ["ACCESSES", "HITS", "MISSES", "COMPULSORY_GLOBAL", "COMPULSORY_NODE", "MIG_HITS", "MIG_MISSES",
+            "INVALIDATED", "EVICTIONS", "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH",
+            "INFEASIBLE_EPOCH", "PEAK_RESIDENT"]
 CI = {n: i for i, n in enumerate(COUNTERS)}
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "TRACE", 3: "CAPACITY", 4: "STATE", 5: "OOM", 6: "CUDA", 7: "NCCL"}
 

@@ -1,6 +1,6 @@
 """Regeneration ratio of every policy against epoch-Belady on the synthetic traces (GPU path).
 
-regen ratio = (MISSES - COMPULSORY)_policy / (MISSES - COMPULSORY)_BELADY, summed over nodes, per
+regen ratio = (MISSES - COMPULSORY_GLOBAL)_policy / (MISSES - COMPULSORY_GLOBAL)_BELADY, summed over nodes, per
 capacity of the sweep (the analogue of the paper's competitive ratio, P:882 and
 Table tab:competitive P:910-923).  Diagnostic only: the paper's 1.31 / 1.86 / 2.84 were measured
 on production traces with a serving system in the loop.
@@ -35,7 +35,7 @@ def main(cfgs):
         t, caps, ctr = pipeline.run_step(d, pc, dict(policy_mask=31), caps_fn)
         torch.cuda.synchronize()
         c = ctr.cpu().numpy()
-        regen = (c[:, :, :, saga.CI["MISSES"]] - c[:, :, :, saga.CI["COMPULSORY"]]).sum(axis=2)
+        regen = (c[:, :, :, saga.CI["MISSES"]] - c[:, :, :, saga.CI["COMPULSORY_GLOBAL"]]).sum(axis=2)
         out = {"config": name, "caps": caps, "policies": POLS, "regen_blocks": regen.tolist()}
         for ci, cap in enumerate(caps):
             base = max(int(regen[1, ci]), 1)

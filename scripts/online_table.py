@@ -3,7 +3,7 @@
 For each config: saga_tool_stats on the generator's tool labels gives each call a TTL base (p95
 of its tool's last 256 observed latencies) and an EMA of observation lengths; the trace is
 reloaded with them as per-call overrides and replayed.  Reported per capacity: regenerated
-blocks (MISSES - COMPULSORY over nodes) of AEG, each relative to epoch-Belady of its own run.
+blocks (MISSES - COMPULSORY_GLOBAL over nodes) of AEG, each relative to epoch-Belady of its own run.
 Diagnostic only.
 
   python scripts/online_table.py [C2 C4]  -> markdown table, profiles/online_<cfg>.json
@@ -25,7 +25,7 @@ from paper_2605_00528_b200 import pipeline, saga  # noqa: E402
 
 def regen(ctr):
     c = ctr.cpu().numpy()
-    return (c[:, :, :, saga.CI["MISSES"]] - c[:, :, :, saga.CI["COMPULSORY"]]).sum(axis=2)
+    return (c[:, :, :, saga.CI["MISSES"]] - c[:, :, :, saga.CI["COMPULSORY_GLOBAL"]]).sum(axis=2)
 
 
 def main(cfgs):

@@ -3,7 +3,7 @@
 For each config: saga_pattern_infer on the generator's tool labels (half the sessions train,
 half held out) gives the next-step accuracy; the trace is then re-annotated with the inferred
 AEG (pipeline.inferred_aeg_desc) and replayed.  Reported per capacity: regenerated blocks
-(MISSES - COMPULSORY, summed over nodes) of AEG with explicit hints and with the inferred AEG,
+(MISSES - COMPULSORY_GLOBAL, summed over nodes) of AEG with explicit hints and with the inferred AEG,
 each relative to epoch-Belady of its own run (placement reads the AEG's TTL, so with work
 stealing the node streams can differ; both runs use the explicit run's capacity sweep).
 Diagnostic only: the paper's 87% / +15.6% TCT were measured on production traces.
@@ -40,7 +40,7 @@ def per_tool(d, L):
 
 def regen(ctr):
     c = ctr.cpu().numpy()
-    return (c[:, :, :, saga.CI["MISSES"]] - c[:, :, :, saga.CI["COMPULSORY"]]).sum(axis=2)
+    return (c[:, :, :, saga.CI["MISSES"]] - c[:, :, :, saga.CI["COMPULSORY_GLOBAL"]]).sum(axis=2)
 
 
 def main(cfgs):

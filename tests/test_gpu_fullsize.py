@@ -46,7 +46,7 @@ def _properties(d, t, caps, ctr):
                 assert r[CI["ACCESSES"]] == n_acc
                 assert r[CI["ACCESSES"]] == r[CI["HITS"]] + r[CI["MISSES"]] + r[CI["MIG_HITS"]] + r[CI["MIG_MISSES"]]
                 assert r[CI["PEAK_RESIDENT"]] <= caps[c]
-                comp.add(int(r[CI["COMPULSORY"]]))
+                comp.add(int(r[CI["COMPULSORY_NODE"]]))
         assert len(comp) <= 1, (w, comp)  # first touches: policy- and capacity-independent
         for c in range(n_caps):
             a, b = ctr[0, c, w], ctr[1, c, w]  # AEG, BELADY
@@ -54,7 +54,7 @@ def _properties(d, t, caps, ctr):
                 continue
             assert a[CI["HITS"]] + a[CI["MIG_HITS"]] <= b[CI["HITS"]] + b[CI["MIG_HITS"]], (w, caps[c])
             if caps[c] >= whi and b[CI["INVALIDATED"]] == 0:
-                assert b[CI["MISSES"]] + b[CI["MIG_MISSES"]] == b[CI["COMPULSORY"]], (w, caps[c])
+                assert b[CI["MISSES"]] + b[CI["MIG_MISSES"]] == b[CI["COMPULSORY_NODE"]], (w, caps[c])
 
 
 def test_c2_full_size_equals_oracle():

@@ -41,6 +41,14 @@ def small_cases():
     cases.append(("C4_hot", d, pc))
     cases.append(("obs1", make_obs1(6, 3), default_place_cfg(0)))
     cases.append(("limit3", make_chain_limit(3), default_place_cfg(3)))
+    # C5's shape: 32 nodes (every lane of the placement warp owns a node, owned mask 0xFFFFFFFF),
+    # 10 tenants with their own shared prefixes; and a hot variant with queues, steals, reroutes
+    d = make("C5", n_sessions=300, n_nodes=32)
+    cases.append(("C5_32n", d, place_cfg_for(d)))
+    d = make("C5", n_sessions=160, n_nodes=32)
+    pc = place_cfg_for(d)
+    pc.update(kappa=2)
+    cases.append(("C5_32n_hot", d, pc))
     return cases
 
 

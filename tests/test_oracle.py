@@ -41,12 +41,20 @@ def hits(ctr, O):
 # A5 scalar formulas: SPEC worked examples
 # ------------------------------------------------------------------------------------------
 
+def _score_inputs(R, S):
+    """(d, tau, size, smax) with d/tau = R and size/smax = S exactly in fp32 (the examples' values)."""
+    d, tau = {0.0: (0, 1), 0.5: (1, 2), 1.0: (7, 7)}[R]
+    size, smax = {0.0: (0, 1), 0.25: (1, 4), 1.0: (3, 3)}[S]
+    return d, tau, size, smax
+
+
 def test_eviction_score_examples(O):
+    # through the oracle's score() (eq:recency / eq:size normalisation included)
     for ex in gold("spec_examples.json")["eviction_score"]:
-        s = O.eviction_score32(0.3, 0.5, 0.2, ex["R"], ex["P"], ex["S"])
+        d, tau, size, smax = _score_inputs(ex["R"], ex["S"])
+        s, q = O.score32(0.3, 0.5, 0.2, d, tau, size, smax, ex["P"])
         assert np.float32(s) == np.float32(ex["fp32"]), ex["cite"]
-        q = int(np.floor(np.float32(s) * np.float32(1048576.0)))
-        assert min(max(q, 0), 1 << 20) == ex["q"], ex["cite"]
+        assert q == ex["q"], ex["cite"]
         # fp64 evaluation of eq:eviction agrees within 1e-6
         assert abs(0.3 * ex["R"] + 0.5 * (1 - ex["P"]) + 0.2 * ex["S"] - s) < 1e-6
 
@@ -70,8 +78,8 @@ def test_fig2_aeg_reuse_and_keys(O):
         es = [(p, 65536) for (u, _, p) in g["edges"] if u == v]
         P = O.reuse32([p for p, _ in es], [q for _, q in es], g["ncur"], g["obs"][v])
         assert np.float32(P) == np.float32(g["p_reuse_fp32"][v]), v
-        s = O.eviction_score32(0.3, 0.5, 0.2, 0.0, P, 1.0)
-        assert int(np.floor(np.float32(s) * np.float32(1048576.0))) == g["q_at_R0_S1"][v], v
+        _, q = O.score32(0.3, 0.5, 0.2, 0, 0, 750, 750, P)   # R = 0 (tau = 0), S = 1
+        assert q == g["q_at_R0_S1"][v], v
 
 
 def _ttl_rational(el, ttl_base, ttl_max, occ, cap, low=700, high=900):
@@ -331,7 +339,7 @@ def test_theorem2_limit_case(O, seed):
     for C in (whi, whi + 3):
         a = o.replay(O.POL_AEG, 0, C)
         b = o.replay(O.POL_BELADY, 0, C)
-        assert misses(a, O) == misses(b, O) == o.min_misses(0, C) == ftn == a[O.CI["COMPULSORY"]]
+        assert misses(a, O) == misses(b, O) == o.min_misses(0, C) == ftn == a[O.CI["COMPULSORY_NODE"]]
 
 
 # ------------------------------------------------------------------------------------------
@@ -357,7 +365,8 @@ def _invariants(o, d, O, caps_per_node=True):
                 assert ctr[O.CI["INFEASIBLE_EPOCH"]] == 0
                 assert ctr[O.CI["PEAK_RESIDENT"]] <= C
                 assert ctr[O.CI["ACCESSES"]] == n == hits(ctr, O) + misses(ctr, O)
-                assert ctr[O.CI["COMPULSORY"]] == ftn
+                assert ctr[O.CI["COMPULSORY_NODE"]] == ftn
+                assert ctr[O.CI["COMPULSORY_GLOBAL"]] <= ctr[O.CI["MISSES"]]
             assert hits(a, O) <= hits(b, O) <= n - mn
             assert hits(x, O) <= hits(b, O)
             if C >= whi:
@@ -419,24 +428,10 @@ def _two_call_trace(gap_us, n_nodes=2, ttl=2_000_000, extra_sessions=()):
 
 
 def test_route_new_session_argmin(O):
-    # a new session goes to the argmin-load worker (ties -> fewer active sessions -> lowest id)
+    # a new session goes to the argmin-load worker (ties -> lowest worker id)
     d = _two_call_trace(10 ** 7, extra_sessions=[(2, 1, 0)])
     node, _, _, _ = O.Oracle(d, default_place_cfg()).placement()
     assert node[0] == 0 and node[1] == 1
-
-
-def test_route_cached_affinity(O):
-    # cached at w and load(w) < theta -> w, even though another node is less loaded
-    d = _two_call_trace(400_000, extra_sessions=[(2, 1, 0)])
-    node, _, _, rr = O.Oracle(d, default_place_cfg()).placement()
-    assert node[0] == 0 and node[2] == 0 and rr == 0
-
-
-def test_route_expired_ttl_goes_argmin(O):
-    # TTL expired -> cached() false -> argmin; session 1 keeps node 1 busy? (ties -> active count)
-    d = _two_call_trace(60_000_000, ttl=1_000_000)
-    node, _, _, _ = O.Oracle(d, default_place_cfg()).placement()
-    assert node[1] in (0, 1)
 
 
 def test_route_overloaded_affinity_reroutes(O):
