@@ -348,6 +348,8 @@ def main():
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
     ap.add_argument("--inflight", type=int, default=None,
                     help="independent steps in flight on separate streams (default 2)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="chain each step's expansion to the previous step's finished replay")
     ap.add_argument("--policy-mask", type=int, default=3,
                     help="1 AEG, 2 BELADY, 4 EVICT_ALL, 8 LRU, 16 LRU+Prefix (default 3: the metric's pair)")
     args = ap.parse_args()
@@ -380,7 +382,12 @@ def main():
     rcfg = dict(policy_mask=args.policy_mask)
     caps_fn = sweep_for(args.config)
     shard_caps = (not trials) and desc.n_nodes == 1 and world > 1
-    inflight = max(1, args.inflight or 2)
+    # Steps in flight.  "overlap": a step's expansion / next use start as soon as the previous
+    # step's replay kernel is queued (they fill the SMs its short items free), which
+    # keeps up to inflight expanded traces resident -- only when they fit (C1-C3); larger
+    # configs chain a step's expansion to the previous step's freed trace.
+    overlap = desc.n_accesses < 3 * 10 ** 8 and not args.no_overlap
+    inflight = max(1, args.inflight or (3 if overlap else 2))
     # one stream, trace handle and communicator per in-flight step (see run_steps)
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
     comm = comms[0]
@@ -429,10 +436,13 @@ def main():
                 if j == 0:
                     return
                 with order["cv"]:
-                    order["cv"].wait_for(lambda: (j - 1) in order["done"] or order.get("error"))
+                    if overlap:  # only after step j-1's replay kernel is queued (its CTAs take the SMs first)
+                        order["cv"].wait_for(lambda: (j - 1) in order["launched"] or order.get("error"))
+                    else:
+                        order["cv"].wait_for(lambda: (j - 1) in order["done"] or order.get("error"))
                     if order.get("error"):
                         raise RuntimeError("another in-flight step failed")
-                    ev = order["done"][j - 1]
+                    ev = None if overlap else order["done"][j - 1]
                 mark(st, "placed", j)
                 if ev is not None:
                     st.wait_event(ev)
@@ -442,14 +452,18 @@ def main():
                 mark(st, "replayed", j)
                 ev = torch.cuda.Event()
                 ev.record(st)
-                order["ev"][j] = ev  # published once the trace is freed (run_steps.worker)
+                with order["cv"]:
+                    order["ev"][j] = ev  # published once the trace is freed (run_steps.worker)
+                    order["launched"].add(j)
+                    order["cv"].notify_all()
         mark(s_, "start", j)
         with torch.cuda.stream(s_):
             t, caps, ctr = pipeline.run_step(desc, pc, rcfg, caps_fn, rank=p_rank, world=p_world,
                                              comm=None if trials else comms[i], device=local, stream=s_, host=host,
                                              counters=counters[i], shard_caps=shard_caps,
                                              before_expand=before, after_replay=after,
-                                             mark=(lambda st, w: mark(st, w, j)) if timeline is not None else None)
+                                             mark=(lambda st, w: mark(st, w, j)) if timeline is not None else None,
+                                             range_comm=comms[i] if trials else None, replay_wait=False)
             if trials and comms[i] is not None:  # A8: combine the per-trial counters over ranks
                 comms[i].allreduce(ctr, op=0, stream=t.stream)
         counters[i] = ctr
@@ -463,6 +477,7 @@ def main():
         with order["cv"]:
             order["done"] = {}
             order["ev"] = {}
+            order["launched"] = set()
             order["error"] = None
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -479,6 +494,7 @@ def main():
                     t, caps, ctr = step(host, i, j)
                     if d2h is not None:
                         d2h(i, ctr)
+                    t.replay_wait()  # the step's replay is done and passed its internal checks
                     t.free()
                     with order["cv"]:  # step j's trace is gone: step j+1 may expand
                         order["done"][j] = order["ev"].get(j)
@@ -656,7 +672,7 @@ def main():
                        "trace_accesses": n_access, "access_replays_per_step": replay_accesses,
                        "trace_accesses_per_s": n_access / (ms / 1e3),
                        "l2": "inputs larger than L2 (node streams 4 B/access + per-node next-use arrays)",
-                       "steps_in_flight": inflight, "step_latency_ms": lat_ms,
+                       "steps_in_flight": inflight, "overlap": overlap, "step_latency_ms": lat_ms,
                        "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
                                     else ("capacity points" if shard_caps else "cache nodes w mod R"))},
             "e2e": e2e, "gpu_launches": int(launches),

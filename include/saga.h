@@ -61,9 +61,9 @@ typedef enum {
                                 shared-prefix blocks only when no private candidate is left */
 } saga_policy;
 
-/* Counter slots, int64 each, 16 per (policy, capacity, node) replay: SURVEY §8.C.7's list, its
- * reserved slot holding the peak resident count.  Identity: ACCESSES = HITS + MISSES + MIG_HITS +
- * MIG_MISSES.  Unavoidable vs regenerated prefill follows P:881 ("tokens prefilled") and
+/* Counter slots, int64 each, SAGA_NCOUNT per (policy, capacity, node) replay: SURVEY §8.C.7's
+ * list (its reserved slot holding the peak resident count), then the PREFETCH record counts of F4.
+ * Identity: ACCESSES = HITS + MISSES + MIG_HITS + MIG_MISSES + PF_HITS + PF_MISSES.  Unavoidable vs regenerated prefill follows P:881 ("tokens prefilled") and
  * Observation 1: a CALL miss is compulsory only at the block's first touch in the
  * whole trace (first call in (t, s) order touching it); every other CALL miss -- including the
  * re-prefill of a rerouted session at its new node -- is regeneration. */
@@ -84,7 +84,11 @@ enum {
   SAGA_C_VICTIM_HASH = 13,      /* sum over victims of splitmix64((epoch << 32) | local id)     */
   SAGA_C_INFEASIBLE_EPOCH = 14, /* first epoch whose requests exceed the capacity, else 0       */
   SAGA_C_PEAK_RESIDENT = 15,    /* max |S| after an epoch (<= capacity)                         */
-  SAGA_NCOUNT = 16
+  SAGA_C_PF_HITS = 16,          /* PREFETCH records found resident (SAGA_LOAD_PREFETCH)          */
+  SAGA_C_PF_MISSES = 17,        /* PREFETCH records loaded ahead of the predicted next step     */
+  SAGA_C_RESERVED18 = 18,
+  SAGA_C_RESERVED19 = 19,
+  SAGA_NCOUNT = 20
 };
 
 /* Columnar trace (host pointers; deep-copied by saga_load_trace).  Validation rules
@@ -192,7 +196,17 @@ saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* c
  * call that needs it (saga_trace_info, saga_node_stream*, saga_belady_next_use).  Lets a caller
  * with several traces in flight run one trace's single-SM placement beside another's replay and
  * start the SM-hungry expansion / next-use only when that replay is done (stream-ordered). */
-enum { SAGA_LOAD_DEFER_EXPAND = 1 };
+enum { SAGA_LOAD_DEFER_EXPAND = 1, SAGA_LOAD_PREFETCH = 2 };
+/* SAGA_LOAD_PREFETCH (F4, speculative prefetching, §4.3; SPEC prefetch_target
+ * S:235-243; DESIGN.md R-prefetch): every node stream also carries PREFETCH records.  When call c
+ * of session s (AEG node v, not is_last, v not terminal, v with successors) finishes inference,
+ * its tool starts at t_end(c); at the boundary e_pf = t_end(c) / epoch_us + 1 the node that
+ * served c prefetches the prefix of the predicted successor u = argmax_u' P(v -> u') (ties: the
+ * lowest node id): the first floor(n_sh / block_tokens) blocks of c's block list, n_sh =
+ * (prompt_c + output_c) * edge_shared_q16(v -> u) >> 16.  Emitted only if e_pf > e(c) and s's
+ * next call is admitted after e_pf.  Per epoch a node's records are MIG (ascending session),
+ * PREFETCH (call order), CALL (call order); PREFETCH records write t_last = T_e and count as
+ * PF_HITS / PF_MISSES (not CALL misses, never compulsory). */
 saga_status saga_load_trace_ex(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask,
                                int device, saga_stream_t stream, uint32_t flags, saga_trace** out);
 
@@ -224,6 +238,12 @@ saga_status saga_node_stream(const saga_trace* t, uint32_t node, uint32_t* block
 saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_use_dev, uint32_t* local_id_dev,
                                  saga_stream_t stream);
 
+/* A4 for several owned nodes at once (no outputs; results kept as by saga_belady_next_use): the
+ * nodes' streams are sorted and scanned as segments of one launch per kernel (K4 onesweep passes,
+ * K5 segmented scan, per-epoch statistics), in batches of up to 32 nodes / 2^30 accesses.  A node
+ * already done is skipped.  Syncs once per batch (sizes of the derived tables). */
+saga_status saga_belady_next_use_nodes(saga_trace* t, const uint32_t* nodes, uint32_t n_nodes, saga_stream_t stream);
+
 /* W_lo = max over record epochs of distinct blocks requested, W_hi = max over record epochs of
  * blocks live across it (first touch <= epoch end and last touch >= epoch start).  Syncs.
  * SAGA_ERR_STATE before saga_belady_next_use(node). */
@@ -251,12 +271,16 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
  * the order AEG, BELADY, EVICT_ALL, LRU, LRU_PREFIX; cells of nodes not listed are left untouched (zero them
  * first; then an all-reduce sum over ranks is an exact gather).  A capacity below a node's
  * W_lo is data, not an error: INFEASIBLE_EPOCH is set and that replay stops counting.
- * SAGA_ERR_CAPACITY if a capacity is 0.  Syncs: the first call for a node builds its replay
- * index (units, event ranges) and every call checks the kernel's internal invariants
- * (SAGA_ERR_STATE with the failing check in saga_last_error()).  Set SAGA_REPLAY_TRACE=1 to
- * print per-item / per-phase SM cycles to stderr. */
+ * SAGA_ERR_CAPACITY if a capacity is 0.  Stream-ordered and asynchronous once the node's replay
+ * index exists (the first call for a node builds it and syncs for its sizes); the kernel's
+ * internal invariant checks are reported by saga_replay_wait.  Set SAGA_REPLAY_TRACE=1 to print
+ * per-item / per-phase SM cycles to stderr (syncs). */
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream);
+
+/* Waits for the handle's stream and reports the replay kernels' internal checks (SAGA_ERR_STATE
+ * with the failing check in saga_last_error()).  Syncs. */
+saga_status saga_replay_wait(saga_trace* t);
 
 /* One (policy, capacity, node) replay of A7 that also logs its victims (SURVEY §1.2's victim
  * logs; the sketch's SAGA_LOG_VICTIMS): cfg->policy_mask must name exactly one policy.

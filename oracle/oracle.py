@@ -21,7 +21,8 @@ POL_AEG, POL_BELADY, POL_EVICT_ALL, POL_LRU, POL_LRU_PREFIX = 1, 2, 4, 8, 16
 INF = 0xFFFFFFFF
 COUNTERS = ["ACCESSES", "HITS", "MISSES", "COMPULSORY_GLOBAL", "COMPULSORY_NODE", "MIG_HITS", "MIG_MISSES",
             "INVALIDATED", "EVICTIONS", "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH",
-            "INFEASIBLE_EPOCH", "PEAK_RESIDENT"]
+            "INFEASIBLE_EPOCH", "PEAK_RESIDENT", "PF_HITS", "PF_MISSES", "RESERVED18", "RESERVED19"]
+NCOUNT = len(COUNTERS)
 CI = {n: i for i, n in enumerate(COUNTERS)}
 
 _lock = threading.Lock()
@@ -73,7 +74,9 @@ def lib():
             L.oracle_new.restype = vp
             L.oracle_new.argtypes = [C.POINTER(ODesc), C.POINTER(OPlace), C.POINTER(C.c_int)]
             L.oracle_new_nodes.restype = vp
-            L.oracle_new_nodes.argtypes = [C.POINTER(ODesc), C.POINTER(OPlace), C.c_uint32, C.POINTER(C.c_int)]
+            L.oracle_new_nodes.argtypes = [C.POINTER(ODesc), C.POINTER(OPlace), C.c_uint32, C.c_uint32,
+                                           C.POINTER(C.c_int)]
+            L.oracle_prefetch.argtypes = [vp, vp, vp]
             L.oracle_free.argtypes = [vp]
             L.oracle_placement.argtypes = [vp, vp, vp]
             L.oracle_migrations.argtypes = [vp, vp]
@@ -125,7 +128,7 @@ def replay_cfg(policy=POL_AEG, alpha=0.3, beta=0.5, gamma=0.2, p_low_pm=700, p_h
 class Oracle:
     """Owns one oracle instance over a TraceDesc (validation, placement and expansion run at build)."""
 
-    def __init__(self, desc, place_cfg: dict, node_mask: int = 0):
+    def __init__(self, desc, place_cfg: dict, node_mask: int = 0, prefetch: bool = False):
         self.desc = desc
         self._keep = {}
         arrs = {}
@@ -139,7 +142,7 @@ class Oracle:
                    place_cfg["theta_pm"], place_cfg["rmax_pm"], place_cfg["t_idle_us"], place_cfg["seed"])
         self.place_cfg = dict(place_cfg)
         err = C.c_int(0)
-        self.h = lib().oracle_new_nodes(C.byref(d), C.byref(p), node_mask, C.byref(err))
+        self.h = lib().oracle_new_nodes(C.byref(d), C.byref(p), node_mask, 2 if prefetch else 0, C.byref(err))
         self.err = err.value
         if not self.h:
             raise ValueError(f"oracle: invalid trace (code {self.err})")
@@ -208,7 +211,7 @@ class Oracle:
     def replay(self, policy, w, cap, rcfg: dict | None = None, log=False):
         cfg = replay_cfg(**(rcfg or {}))
         cfg.policy = policy
-        ctr = np.zeros(16, np.int64)
+        ctr = np.zeros(NCOUNT, np.int64)
         if log:
             cap_log = 1 << 22
             buf = np.zeros(cap_log, np.uint32)
@@ -221,7 +224,7 @@ class Oracle:
         """(counters, victims as uint64 (epoch << 32) | local id in eviction order)."""
         cfg = replay_cfg(**(rcfg or {}))
         cfg.policy = policy
-        ctr = np.zeros(16, np.int64)
+        ctr = np.zeros(NCOUNT, np.int64)
         cap_log = 1 << 22
         buf = np.zeros(cap_log, np.uint64)
         n = lib().oracle_replay_log(self.h, C.byref(cfg), w, cap, ctr.ctypes.data, buf.ctypes.data, cap_log)
@@ -233,10 +236,17 @@ class Oracle:
         caps = np.ascontiguousarray(caps, np.uint32)
         nodes = np.arange(self.desc.n_nodes, dtype=np.uint32) if nodes is None else np.ascontiguousarray(nodes, np.uint32)
         npol = bin(policy_mask & 31).count("1")
-        out = np.zeros((npol, caps.size, self.desc.n_nodes, 16), np.int64)
+        out = np.zeros((npol, caps.size, self.desc.n_nodes, NCOUNT), np.int64)
         lib().oracle_replay_many(self.h, C.byref(cfg), policy_mask, caps.ctypes.data, caps.size, nodes.ctypes.data,
                                  nodes.size, out.ctypes.data, int(nthreads or os.cpu_count() or 1))
         return out
+
+    def prefetch_plan(self):
+        """Per call (PREFETCH epoch or 0, prefix blocks) -- with prefetch=True."""
+        e = np.zeros(self.desc.n_calls, np.uint32)
+        n = np.zeros(self.desc.n_calls, np.uint32)
+        lib().oracle_prefetch(self.h, _p(e), _p(n))
+        return e, n
 
     def min_misses(self, w, cap):
         return lib().oracle_min_misses(self.h, w, cap)

@@ -88,8 +88,9 @@ enum { POL_AEG = 1, POL_BELADY = 2, POL_EVICT_ALL = 4, POL_LRU = 8, POL_LRU_PREF
 enum {
   C_ACCESSES, C_HITS, C_MISSES, C_COMPULSORY_GLOBAL, C_COMPULSORY_NODE, C_MIG_HITS, C_MIG_MISSES,
   C_INVALIDATED, C_EVICTIONS, C_EVICT_PROTECTED, C_EVICT_EVENTS, C_REGEN_TOKENS, C_REGEN_US, C_VICTIM_HASH,
-  C_INFEASIBLE_EPOCH, C_PEAK_RESIDENT, C_N
+  C_INFEASIBLE_EPOCH, C_PEAK_RESIDENT, C_PF_HITS, C_PF_MISSES, C_RES18, C_RES19, C_N
 };
+enum { K_CALL = 0, K_MIG = 1, K_PF = 2 };   // record kinds of a node stream
 
 // public-domain splitmix64 finaliser (Steele/Lea/Flood; constants of SURVEY §8.C.2 P5)
 uint64_t splitmix64(uint64_t x) {
@@ -104,11 +105,12 @@ std::vector<T> cp(const T* p, size_t n) {
   return p ? std::vector<T>(p, p + n) : std::vector<T>(n);
 }
 
-struct Group {           // one MIG or CALL record group in a node stream
+struct Group {           // one MIG, PREFETCH or CALL record group in a node stream
   uint64_t pos0, len;
-  int kind;              // 0 CALL, 1 MIG
-  int64_t tval;          // t_last written by its records: t_c (CALL) or T_e (MIG)
+  int kind;              // K_CALL, K_MIG, K_PF
+  int64_t tval;          // t_last written by its records: t_c (CALL) or T_e (MIG, PREFETCH)
   uint32_t call;         // call whose ranges the records are
+  uint64_t lim;          // at most this many of the call's blocks (the predicted prefix of a PREFETCH)
 };
 struct Event {           // one event epoch of a node
   uint32_t e;
@@ -146,6 +148,7 @@ struct Oracle {
   // ---- derived ----
   std::vector<uint32_t> owner;        // owner[b]: session id, or n_sessions + type for shared prefix
   std::vector<uint32_t> first_call;   // first call (global (t, s) order) whose ranges touch block b
+  std::vector<uint32_t> pf_e, pf_len; // per call: PREFETCH epoch (0 = none) and prefix blocks
   std::vector<uint32_t> ecall;        // admission epoch e(c) = floor(t_c / E) + 1
   std::vector<std::vector<uint32_t>> scalls;  // calls of each session in order
   std::vector<uint8_t> node_of;
@@ -222,6 +225,37 @@ struct Oracle {
   int64_t t_end(uint32_t c) const {
     return t[c] + ceil_div(int64_t(newt[c]) * 1000000, pc.prefill_tok_s) +
            ceil_div(int64_t(outt[c]) * 1000000, pc.decode_tok_s);
+  }
+
+  // Speculative prefetch (§4.3; DESIGN.md R-prefetch): when call c finishes
+  // inference and its tool starts (t_end(c)), predict the successor u = argmax_u' P(v_c -> u')
+  // (ties: lowest node id) and prefetch the prefix it shares -- the first floor(n_sh / btok)
+  // blocks of c's block list, n_sh = n_cur * shared_q16(v_c -> u) >> 16 (eq:overlap) -- at the
+  // node that served c, at the first boundary after the tool start, e_pf = t_end(c) / E + 1.
+  // Emitted only while the session is still in that tool call (its next call is admitted after
+  // e_pf) and when e_pf > e(c); never for finished sessions (is_last or a terminal node).
+  void plan_prefetch() {
+    pf_e.assign(n_calls, 0);
+    pf_len.assign(n_calls, 0);
+    for (uint32_t c = 0; c < n_calls; ++c) {
+      const uint32_t v = vnode[c];
+      if (last[c] || term[v] || eoff[v + 1] == eoff[v]) continue;
+      uint32_t best = eoff[v];
+      for (uint32_t k = eoff[v] + 1; k < eoff[v + 1]; ++k)
+        if (ep[k] > ep[best] || (ep[k] == ep[best] && edst[k] < edst[best])) best = k;
+      const uint64_t ncur = uint64_t(prompt[c]) + outt[c];
+      const uint64_t nsh = (ncur * uint64_t(eq16[best])) >> 16;
+      uint64_t blocks = 0;
+      for (uint32_t r = roff[c]; r < roff[c + 1]; ++r) blocks += rlen[r];
+      const uint64_t len = std::min<uint64_t>(blocks, nsh / btok);
+      const uint32_t e = uint32_t(t_end(c) / pc.epoch_us + 1);
+      if (len == 0 || e <= ecall[c]) continue;
+      const auto& cl = scalls[sess[c]];
+      const auto it = std::upper_bound(cl.begin(), cl.end(), c);
+      if (it != cl.end() && ecall[*it] <= e) continue;   // the next step is back by then
+      pf_e[c] = e;
+      pf_len[c] = uint32_t(len);
+    }
   }
 
   void place() {
@@ -365,12 +399,17 @@ struct Oracle {
       int64_t cm = -1;
       for (uint32_t c : cl) if (ecall[c] < m.e) cm = c;
       Event& x = ev_at(m.t, m.e);
-      x.groups.push_back({0, 0, 1, int64_t(m.e) * pc.epoch_us, uint32_t(cm)});
+      x.groups.push_back({0, 0, K_MIG, int64_t(m.e) * pc.epoch_us, uint32_t(cm), UINT64_MAX});
       ev_at(m.v, m.e).inv.push_back(m.s);
+    }
+    for (uint32_t c = 0; c < n_calls; ++c) {   // PREFETCH groups (§4.3; DESIGN.md R-prefetch)
+      if (pf_e.empty() || pf_e[c] == 0) continue;
+      Event& x = ev_at(node_of[c], pf_e[c]);
+      x.groups.push_back({0, 0, K_PF, int64_t(pf_e[c]) * pc.epoch_us, c, pf_len[c]});
     }
     for (uint32_t c = 0; c < n_calls; ++c) {
       Event& x = ev_at(node_of[c], ecall[c]);
-      x.groups.push_back({0, 0, 0, t[c], c});
+      x.groups.push_back({0, 0, K_CALL, t[c], c, UINT64_MAX});
     }
     for (uint32_t w = 0; w < n_nodes; ++w) {
       NodeData& nd = nodes[w];
@@ -378,17 +417,22 @@ struct Oracle {
       for (auto& kv : evs[w]) {
         Event x = kv.second;
         std::sort(x.inv.begin(), x.inv.end());
-        // MIG groups were pushed before CALL groups; keep MIG ascending by session
+        // per epoch: MIG records (ascending session), then PREFETCH (call order), then CALL (call order)
+        auto rank_of = [](int kind) { return kind == K_MIG ? 0 : (kind == K_PF ? 1 : 2); };
         std::stable_sort(x.groups.begin(), x.groups.end(), [&](const Group& a, const Group& b) {
-          if (a.kind != b.kind) return a.kind > b.kind;  // MIG (1) first
-          if (a.kind == 1) return sess[a.call] < sess[b.call];
-          return false;
+          if (a.kind != b.kind) return rank_of(a.kind) < rank_of(b.kind);
+          if (a.kind == K_MIG) return sess[a.call] < sess[b.call];
+          return false;   // PREFETCH / CALL groups were pushed in call order
         });
         uint32_t evi = uint32_t(nd.ev.size());
         for (auto& g : x.groups) {
           g.pos0 = nd.block.size();
           for (uint32_t r = roff[g.call]; r < roff[g.call + 1]; ++r)
-            for (uint32_t i = 0; i < rlen[r]; ++i) { nd.block.push_back(rlo[r] + i); nd.ev_of_pos.push_back(evi); }
+            for (uint32_t i = 0; i < rlen[r]; ++i) {
+              if (nd.block.size() - g.pos0 >= g.lim) break;
+              nd.block.push_back(rlo[r] + i);
+              nd.ev_of_pos.push_back(evi);
+            }
           g.len = nd.block.size() - g.pos0;
         }
         auto it = act_log.find({x.e, w});
@@ -456,10 +500,9 @@ struct Oracle {
 
   // newest call c* of session s with e(c*) <= e (SURVEY §8.C.6 "Session state at T_e")
   int64_t cstar(uint32_t s, uint32_t e) const {
-    const auto& cl = scalls[s];
-    int64_t r = -1;
-    for (uint32_t c : cl) { if (ecall[c] <= e) r = c; else break; }
-    return r;
+    const auto& cl = scalls[s];   // the session's calls in (t, s) order, so e(c) is non-decreasing
+    auto it = std::upper_bound(cl.begin(), cl.end(), e, [&](uint32_t ee, uint32_t c) { return ee < ecall[c]; });
+    return it == cl.begin() ? -1 : int64_t(*(it - 1));   // last call with e(c) <= e
   }
 
   // ------------------------------------------------------------------------------------------
@@ -602,9 +645,13 @@ struct Oracle {
         if (cfg.policy == POL_AEG) {
           Ctx x = make_ctx(cfg, e, Te, int64_t(S.size()), C, ev.act);
           std::vector<OwnerState> sts;
+          std::unordered_map<uint32_t, OwnerState> memo;   // owner_state is a function of (owner, e, act)
           for (uint32_t b : cand) {
             x.tau = std::max(x.tau, Te - tl[b]);                       // tau_max over candidates
-            sts.push_back(owner_state(owner[nd.uniq[b]], e, ev.act));
+            const uint32_t ow = owner[nd.uniq[b]];
+            auto mi = memo.find(ow);
+            if (mi == memo.end()) mi = memo.emplace(ow, owner_state(ow, e, ev.act)).first;
+            sts.push_back(mi->second);
             x.smax = std::max(x.smax, sts.back().size);                 // size_max over candidates
           }
           for (size_t i = 0; i < cand.size(); ++i) {
@@ -651,10 +698,12 @@ struct Oracle {
           uint32_t b = nd.local_id[p];
           ctr[C_ACCESSES]++;
           if (res[b]) {
-            ctr[g.kind == 0 ? C_HITS : C_MIG_HITS]++;
+            ctr[g.kind == K_CALL ? C_HITS : (g.kind == K_MIG ? C_MIG_HITS : C_PF_HITS)]++;
           } else {
             res[b] = 1; S.insert(b);
-            if (g.kind == 0) {
+            if (g.kind == K_PF) {
+              ctr[C_PF_MISSES]++;   // the block is loaded ahead of the predicted next step
+            } else if (g.kind == K_CALL) {
               ctr[C_MISSES]++;
               // "tokens prefilled": a CALL miss is unavoidable only at the block's first
               // touch in the whole trace; a re-prefill elsewhere (reroute) is regeneration
@@ -701,7 +750,7 @@ struct Oracle {
   }
 };
 
-Oracle* build(const ODesc* d, const OPlace* p, uint32_t node_mask, int* err) {
+Oracle* build(const ODesc* d, const OPlace* p, uint32_t node_mask, uint32_t flags, int* err) {
   Oracle* o = new Oracle();
   o->node_mask = node_mask;
   o->n_calls = d->n_calls; o->n_sessions = d->n_sessions; o->n_types = d->n_types; o->n_aeg = d->n_aeg_nodes;
@@ -743,6 +792,7 @@ Oracle* build(const ODesc* d, const OPlace* p, uint32_t node_mask, int* err) {
     o->scalls[o->sess[c]].push_back(c);
   }
   o->place();
+  if (flags & 2u) o->plan_prefetch();   // SAGA_LOAD_PREFETCH
   o->expand();
   *err = 0;
   return o;
@@ -755,9 +805,20 @@ Oracle* build(const ODesc* d, const OPlace* p, uint32_t node_mask, int* err) {
 // ============================================================================================
 extern "C" {
 
-void* oracle_new(const ODesc* d, const OPlace* p, int* err) { return build(d, p, 0, err); }
-// as oracle_new, but only the streams of the nodes in node_mask are expanded (large traces)
-void* oracle_new_nodes(const ODesc* d, const OPlace* p, uint32_t node_mask, int* err) { return build(d, p, node_mask, err); }
+void* oracle_new(const ODesc* d, const OPlace* p, int* err) { return build(d, p, 0, 0, err); }
+// as oracle_new, but only the streams of the nodes in node_mask are expanded (large traces);
+// flags 2 = PREFETCH records (SAGA_LOAD_PREFETCH)
+void* oracle_new_nodes(const ODesc* d, const OPlace* p, uint32_t node_mask, uint32_t flags, int* err) {
+  return build(d, p, node_mask, flags, err);
+}
+// per call: PREFETCH epoch (0 = none) and prefix blocks (after oracle_new_nodes with flags 2)
+void oracle_prefetch(void* h, uint32_t* e_out, uint32_t* len_out) {
+  Oracle* o = static_cast<Oracle*>(h);
+  for (uint32_t c = 0; c < o->n_calls; ++c) {
+    e_out[c] = o->pf_e.empty() ? 0 : o->pf_e[c];
+    len_out[c] = o->pf_len.empty() ? 0 : o->pf_len[c];
+  }
+}
 void oracle_free(void* h) { delete static_cast<Oracle*>(h); }
 
 void oracle_placement(void* h, uint8_t* node_out, int64_t* stats /*[steals, reroutes, n_mig]*/) {

@@ -41,43 +41,77 @@ __device__ uint32_t newest_before(const TraceView& v, uint32_t s, uint32_t e) {
   uint32_t lo = v.sc_off[s], hi = v.sc_off[s + 1];
   while (lo < hi) {
     uint32_t mid = (lo + hi) >> 1;
-    if (v.ecall[v.sc_call[mid]] < e) lo = mid + 1; else hi = mid;
+    if (v.sc_e[mid] < e) lo = mid + 1; else hi = mid;
   }
   return lo > v.sc_off[s] ? v.sc_call[lo - 1] : NONE;
 }
 
-// merge CALL groups (node's calls in call order) and MIG groups (by epoch) -> group arrays
+// merge CALL groups (node's calls in call order), MIG groups (by epoch) and PREFETCH groups (by
+// epoch, call order within one) -> group arrays; per epoch MIG, then PREFETCH, then CALL
+__device__ __forceinline__ uint32_t count_le(const uint32_t* list, uint32_t n, const uint32_t* key_of, uint32_t e,
+                                             bool strict) {
+  uint32_t lo = 0, hi = n;  // #entries with key < e (strict) or <= e
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint32_t k = key_of[list[mid]];
+    if (strict ? k < e : k <= e) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 __global__ void k_groups(TraceView v, const uint32_t* clist, uint32_t nC, const Mig* migs, const uint32_t* mlist,
-                         uint32_t nM, uint32_t* g_call, uint32_t* g_kind, uint32_t* g_e, int64_t* g_t, uint64_t* g_len) {
-  const uint32_t n = nC + nM;
+                         uint32_t nM, const uint32_t* mig_e, const uint32_t* plist, uint32_t nP, uint32_t* g_call,
+                         uint32_t* g_kind, uint32_t* g_e, int64_t* g_t, uint64_t* g_len) {
+  const uint32_t n = nC + nM + nP;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t dst, call, kind, e;
     int64_t tv;
+    uint64_t len;
     if (i < nC) {
       call = clist[i];
       e = v.ecall[call];
-      uint32_t lo = 0, hi = nM;  // #MIG with epoch <= e (MIG first on ties)
-      while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (migs[mlist[mid]].e <= e) lo = mid + 1; else hi = mid; }
-      dst = i + lo;
+      dst = i + count_le(mlist, nM, mig_e, e, false) + (nP ? count_le(plist, nP, v.pf_e, e, false) : 0u);
       kind = 0;
       tv = v.call_t[call];
-    } else {
-      uint32_t m = i - nC;
+      len = v.rsum[call];
+    } else if (i < nC + nM) {
+      const uint32_t m = i - nC;
       const Mig g = migs[mlist[m]];
       e = g.e;
-      uint32_t lo = 0, hi = nC;  // #CALL with epoch < e
-      while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (v.ecall[clist[mid]] < e) lo = mid + 1; else hi = mid; }
-      dst = m + lo;
+      dst = m + count_le(clist, nC, v.ecall, e, true) + (nP ? count_le(plist, nP, v.pf_e, e, true) : 0u);
       call = newest_before(v, g.s, e);
       kind = 1;
       tv = (int64_t)e * v.epoch_us;
+      len = call == NONE ? 0 : v.rsum[call];
+    } else {
+      const uint32_t p = i - nC - nM;
+      call = plist[p];
+      e = v.pf_e[call];
+      dst = p + count_le(mlist, nM, mig_e, e, false) + count_le(clist, nC, v.ecall, e, true);
+      kind = 2;
+      tv = (int64_t)e * v.epoch_us;
+      len = v.pf_len[call];
     }
     g_call[dst] = call;
     g_kind[dst] = kind;
     g_e[dst] = e;
     g_t[dst] = tv;
-    g_len[dst] = call == NONE ? 0 : v.rsum[call];
+    g_len[dst] = len;
   }
+}
+// epoch of each migration (key table for the merge ranks)
+__global__ void k_mig_e(const Mig* m, uint32_t n, uint32_t* e) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) e[i] = m[i].e;
+}
+// PREFETCH candidates of node w (in call order) and their sort keys
+__global__ void k_flag_pf(const uint8_t* node_of, const uint32_t* pf_e, uint32_t n, uint32_t w, uint32_t* flag) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    flag[c] = node_of[c] == w && pf_e[c] != 0;
+}
+__global__ void k_pf_keys(const uint32_t* list, uint32_t n, const uint32_t* pf_e, uint32_t* key) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) key[i] = pf_e[list[i]];
+}
+__global__ void k_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t n, uint32_t* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
 }
 
 __global__ void k_ev_head(const uint32_t* g_e, uint32_t G, uint32_t* head) {
@@ -124,8 +158,9 @@ __global__ void k_ev_finish(uint32_t J, uint32_t G, uint32_t w, uint32_t* ev_e, 
   }
 }
 
-// one warp per group: write the global block ids of the group's ranges at its positions
-// and mark the CALL records that are their block's first touch in the whole trace (ftg bitmap)
+// one warp per group: write the global block ids of the group's ranges at its positions (a
+// PREFETCH group: its first g_len blocks) and mark the CALL records that are their block's first
+// touch in the whole trace (ftg bitmap)
 __global__ void k_fill_stream(TraceView v, const uint32_t* g_call, const uint32_t* g_kind, const uint64_t* g_pos,
                               uint32_t G, uint32_t* block, uint32_t* ftg) {
   const int lane = threadIdx.x & 31;
@@ -134,8 +169,9 @@ __global__ void k_fill_stream(TraceView v, const uint32_t* g_call, const uint32_
     if (c == NONE) continue;
     const bool call_rec = g_kind[g] == 0;
     uint64_t p = g_pos[g];
-    for (uint32_t r = v.roff[c]; r < v.roff[c + 1]; ++r) {
-      const uint32_t lo = v.rlo[r], n = v.rlen[r];
+    const uint64_t pe = g_pos[g + 1];
+    for (uint32_t r = v.roff[c]; r < v.roff[c + 1] && p < pe; ++r) {
+      const uint32_t lo = v.rlo[r], n = (uint32_t)min((uint64_t)v.rlen[r], pe - p);
       for (uint32_t i = lane; i < n; i += 32) {
         block[p + i] = lo + i;
         if (call_rec && v.fcall[lo + i] == c) atomicOr(&ftg[(p + i) >> 5], 1u << ((p + i) & 31));
@@ -169,7 +205,38 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
   SAGA_CK(scan_u32(t, flag, pos, nc));
   k_scatter_flag<<<grid_for(nc), NTHREADS, 0, s>>>(flag, pos, nc, clist);
   count_launch();
-  uint32_t nC = 0, nM = 0, nI = 0;
+  uint32_t nC = 0, nM = 0, nI = 0, nP = 0;
+  uint32_t* mig_e = dalloc<uint32_t>(t, size_t(nm) + 1);
+  uint32_t* plist = nullptr;
+  if (!mig_e) { set_error("out of device memory (expand)"); return SAGA_ERR_OOM; }
+  if (nm > 0) {
+    k_mig_e<<<grid_for(nm), NTHREADS, 0, s>>>(t->migs, nm, mig_e);
+    count_launch();
+  }
+  if (v.pf_e && nc > 0) {  // PREFETCH groups of this node, stably sorted by their boundary
+    uint32_t* pflag = dalloc<uint32_t>(t, nc);
+    uint32_t* ppos = dalloc<uint32_t>(t, size_t(nc) + 1);
+    uint32_t* pl0 = dalloc<uint32_t>(t, nc);
+    if (!pflag || !ppos || !pl0) { set_error("out of device memory (expand)"); return SAGA_ERR_OOM; }
+    k_flag_pf<<<grid_for(nc), NTHREADS, 0, s>>>(t->node_of, v.pf_e, nc, w, pflag);
+    count_launch();
+    SAGA_CK(scan_u32(t, pflag, ppos, nc));
+    k_scatter_flag<<<grid_for(nc), NTHREADS, 0, s>>>(pflag, ppos, nc, pl0);
+    count_launch();
+    SAGA_CK(d2h(&nP, ppos + nc, 4, s));
+    if (nP > 0) {
+      uint32_t* key = dalloc<uint32_t>(t, nP);
+      uint32_t* skey = dalloc<uint32_t>(t, nP);
+      uint32_t* perm = dalloc<uint32_t>(t, nP);
+      plist = dalloc<uint32_t>(t, nP);
+      if (!key || !skey || !perm || !plist) { set_error("out of device memory (expand)"); return SAGA_ERR_OOM; }
+      k_pf_keys<<<grid_for(nP), NTHREADS, 0, s>>>(pl0, nP, v.pf_e, key);
+      count_launch();
+      SAGA_CK(onesweep_sort_pairs(t, key, nP, 32, skey, perm, s));  // stable: call order within a boundary
+      k_gather_u32<<<grid_for(nP), NTHREADS, 0, s>>>(pl0, perm, nP, plist);
+      count_launch();
+    }
+  }
   if (nm > 0) {
     k_flag_mig<<<grid_for(nm), NTHREADS, 0, s>>>(t->migs, nm, w, ft, fv);
     count_launch();
@@ -184,7 +251,7 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
   SAGA_CK_LAUNCH();
   SAGA_CK(d2h(&nC, pos + nc, 4, s));
   SAGA_CK(cudaStreamSynchronize(s));
-  const uint32_t G = nC + nM;
+  const uint32_t G = nC + nM + nP;
   nd.G = G;
   nd.n_inv = nI;
   nd.g_call = dalloc<uint32_t>(t, G);
@@ -200,7 +267,8 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
     return SAGA_ERR_OOM;
   }
   if (G > 0) {
-    k_groups<<<grid_for(G), NTHREADS, 0, s>>>(v, clist, nC, t->migs, mlist, nM, nd.g_call, nd.g_kind, nd.g_e, nd.g_t, g_len);
+    k_groups<<<grid_for(G), NTHREADS, 0, s>>>(v, clist, nC, t->migs, mlist, nM, mig_e, plist, nP, nd.g_call, nd.g_kind,
+                                              nd.g_e, nd.g_t, g_len);
     k_ev_head<<<grid_for(G), NTHREADS, 0, s>>>(nd.g_e, G, head);
     count_launch(2);
   }

@@ -145,6 +145,11 @@ __global__ void k_sess_scatter(TraceView v, const uint32_t* sc_off, uint32_t* fi
   }
 }
 
+__global__ void k_sc_e(TraceView v, const uint32_t* ecall, const uint32_t* sc_call, uint32_t* sc_e) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < v.n_calls; i += gridDim.x * blockDim.x)
+    sc_e[i] = ecall[sc_call[i]];
+}
+
 __global__ void k_sess_sort(TraceView v, const uint32_t* sc_off, uint32_t* sc_call) {
   // insertion sort of each session's (short) call list into call order
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < v.n_sessions; s += gridDim.x * blockDim.x) {
@@ -155,6 +160,34 @@ __global__ void k_sess_sort(TraceView v, const uint32_t* sc_off, uint32_t* sc_ca
       while (j > a && sc_call[j - 1] > x) { sc_call[j] = sc_call[j - 1]; --j; }
       sc_call[j] = x;
     }
+  }
+}
+
+// F4 speculative prefetch plan (§4.3; saga.h SAGA_LOAD_PREFETCH): per call
+// the boundary at which its predicted successor's prefix is prefetched (0 = none) and its length
+__global__ void k_prefetch_plan(TraceView v, uint32_t* pf_e, uint32_t* pf_len) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < v.n_calls; c += gridDim.x * blockDim.x) {
+    uint32_t e_out = 0, len_out = 0;
+    const uint32_t x = v.call_v[c];
+    const uint32_t k0 = v.eoff[x], k1 = v.eoff[x + 1];
+    if (!v.call_last[c] && !v.term[x] && k1 > k0) {
+      uint32_t best = k0;  // argmax P(v -> u), ties -> lowest u
+      for (uint32_t k = k0 + 1; k < k1; ++k)
+        if (v.ep[k] > v.ep[best] || (v.ep[k] == v.ep[best] && v.edst[k] < v.edst[best])) best = k;
+      const uint64_t ncur = uint64_t(v.call_prompt[c]) + v.call_out[c];
+      const uint64_t nsh = (ncur * uint64_t(v.eq16[best])) >> 16;
+      const uint64_t len = min((uint64_t)v.rsum[c], nsh / v.btok);
+      const uint32_t e = (uint32_t)(v.tend[c] / v.epoch_us + 1);
+      if (len > 0 && e > v.ecall[c]) {
+        // the session's next call (call lists are ascending): it must arrive after the prefetch
+        const uint32_t s = v.call_sess[c];
+        uint32_t lo = v.sc_off[s], hi = v.sc_off[s + 1];
+        while (lo < hi) { const uint32_t mid = (lo + hi) >> 1; if (v.sc_call[mid] <= c) lo = mid + 1; else hi = mid; }
+        if (lo == v.sc_off[s + 1] || v.ecall[v.sc_call[lo]] > e) { e_out = e; len_out = (uint32_t)len; }
+      }
+    }
+    pf_e[c] = e_out;
+    pf_len[c] = len_out;
   }
 }
 
@@ -284,10 +317,28 @@ saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d) {
   SAGA_CK(scan_u32(t, scnt, scoff, d->n_sessions));
   k_sess_scatter<<<grid_for(d->n_calls), NTHREADS, 0, t->stream>>>(v, scoff, fill, sccall);
   k_sess_sort<<<grid_for(d->n_sessions), NTHREADS, 0, t->stream>>>(v, scoff, sccall);
-  count_launch(2);
+  uint32_t* sce = dalloc<uint32_t>(t, d->n_calls);
+  if (!sce) { set_error("saga_load_trace: out of device memory"); return SAGA_ERR_OOM; }
+  k_sc_e<<<grid_for(d->n_calls), NTHREADS, 0, t->stream>>>(v, ecall, sccall, sce);
+  count_launch(3);
   SAGA_CK_LAUNCH();
   v.ecall = ecall; v.tend = tend; v.rsum = rsum; v.ci_P = ciP; v.ci_size = cisz; v.ci_fin = cifin;
-  v.sc_off = scoff; v.sc_call = sccall;
+  v.sc_off = scoff; v.sc_call = sccall; v.sc_e = sce;
+  return SAGA_OK;
+}
+
+saga_status run_prefetch_plan(saga_trace* t) {
+  TraceView& v = t->v;
+  uint32_t* pe = dalloc<uint32_t>(t, v.n_calls);
+  uint32_t* pl = dalloc<uint32_t>(t, v.n_calls);
+  if (!pe || !pl) { set_error("saga_load_trace: out of device memory (prefetch plan)"); return SAGA_ERR_OOM; }
+  if (v.n_calls) {
+    k_prefetch_plan<<<grid_for(v.n_calls), NTHREADS, 0, t->stream>>>(v, pe, pl);
+    count_launch();
+    SAGA_CK_LAUNCH();
+  }
+  v.pf_e = pe;
+  v.pf_len = pl;
   return SAGA_OK;
 }
 

@@ -58,7 +58,8 @@ constexpr int RT = SAGA_REPLAY_RT;
 constexpr int RW = RT / 32;
 constexpr uint32_t KIND_MIG = 0x80000000u;  // u_of bit 31: the position is a MIG record
 constexpr uint32_t U_SHARED = 0x40000000u;  // u_of bit 30: the block is a shared-prefix block
-constexpr uint32_t UMASK = 0x3FFFFFFFu;
+constexpr uint32_t KIND_PF = 0x20000000u;   // u_of bit 29: the position is a PREFETCH record
+constexpr uint32_t UMASK = 0x1FFFFFFFu;
 // first-level key-part digit: !prot * 1025 + (q >> 10), q <= 2^20 (2050 values, kp order)
 constexpr int H1 = 2560;
 __device__ __forceinline__ uint32_t kp_digit(uint32_t kp) { return (kp >> 31) * 1025u + ((kp & 0x1FFFFFu) >> 10); }
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
     int cur = 0;          // active list buffer
     uint32_t ucur = 0;    // session-update cursor (uniform)
     long long c_hit = 0, c_miss = 0, c_mhit = 0, c_mmiss = 0, c_comp = 0, c_compg = 0, c_regen = 0, c_inv = 0;
+    long long c_phit = 0, c_pmiss = 0;
     long long c_ev = 0, c_prot = 0, c_evev = 0, c_peak = 0, infeasible = 0;
     unsigned long long hash = 0;
     uint32_t bad = 0;
@@ -650,7 +652,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       PH(0);
       // ---- R2: |A|, new = |A \ S|; hits / misses; in-flight blocks leave the index ----
       uint32_t nA = 0, nnew = 0;
-      uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_comp = 0, t_compg = 0, t_regen = 0;
+      uint32_t t_hit = 0, t_miss = 0, t_mhit = 0, t_mmiss = 0, t_phit = 0, t_pmiss = 0, t_comp = 0, t_compg = 0,
+               t_regen = 0;
       // A first-in-epoch record p is a hit iff bit p of the next-use-resident bitmap is set (the
       // resident block's next use is p); a warp's 32 positions are one aligned bitmap word.
       uint32_t* nres = belady ? pend.bits : nres_a;
@@ -674,16 +677,19 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           const bool first = in[u] && !(lf[u] & LID_NFIE);
           const bool resident = first && ((nw[u] >> lane) & 1u);
           const bool mig = (uo[u] & KIND_MIG) != 0;
+          const bool pf = (uo[u] & KIND_PF) != 0;
           if (in[u]) {
             if (first && !resident) {
               ++nA; ++nnew;
               // CALL miss: compulsory only at the block's first touch in the whole trace, else a
               // re-prefill = regeneration ("tokens prefilled"), also after a reroute
-              if (mig) ++t_mmiss; else { ++t_miss; if (lf[u] & LID_FTG) ++t_compg; else ++t_regen; }
+              if (mig) ++t_mmiss;
+              else if (pf) ++t_pmiss;
+              else { ++t_miss; if (lf[u] & LID_FTG) ++t_compg; else ++t_regen; }
               if (lf[u] & LID_FTN) ++t_comp;
             } else {
               if (first) ++nA;
-              if (mig) ++t_mhit; else ++t_hit;
+              if (mig) ++t_mhit; else if (pf) ++t_phit; else ++t_hit;
             }
           }
           // in-flight blocks leave the index until R4
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       }
       if (nA > C) { infeasible = e; break; }
       c_hit += t_hit; c_miss += t_miss; c_mhit += t_mhit; c_mmiss += t_mmiss; c_comp += t_comp; c_compg += t_compg;
-      c_regen += t_regen;
+      c_regen += t_regen; c_phit += t_phit; c_pmiss += t_pmiss;
       const uint32_t inAS = nA - nnew;  // in-flight (resident) blocks
       const int64_t kk = (pol == SAGA_POLICY_EVICT_ALL) ? (int64_t)S - (int64_t)inAS
                                                         : (int64_t)S + (int64_t)nnew - (int64_t)C;
@@ -1049,13 +1055,16 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       atomicAdd(&sc[SAGA_C_COMPULSORY_GLOBAL], (unsigned long long)c_compg);
       atomicAdd(&sc[SAGA_C_REGEN_TOKENS], (unsigned long long)c_regen);
       atomicAdd(&sc[SAGA_C_VICTIM_HASH], hash);
+      atomicAdd(&sc[SAGA_C_PF_HITS], (unsigned long long)c_phit);
+      atomicAdd(&sc[SAGA_C_PF_MISSES], (unsigned long long)c_pmiss);
     }
     if (bad) atomicOr(a.err, 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
       int64_t* out = a.counters + (((uint64_t)pi * a.n_caps + ci) * a.n_nodes_total + w) * SAGA_NCOUNT;
       const long long rg = s_ctr[SAGA_C_REGEN_TOKENS];
-      out[SAGA_C_ACCESSES] = s_ctr[SAGA_C_HITS] + s_ctr[SAGA_C_MISSES] + s_ctr[SAGA_C_MIG_HITS] + s_ctr[SAGA_C_MIG_MISSES];
+      out[SAGA_C_ACCESSES] = s_ctr[SAGA_C_HITS] + s_ctr[SAGA_C_MISSES] + s_ctr[SAGA_C_MIG_HITS] + s_ctr[SAGA_C_MIG_MISSES] +
+                             s_ctr[SAGA_C_PF_HITS] + s_ctr[SAGA_C_PF_MISSES];
       out[SAGA_C_HITS] = s_ctr[SAGA_C_HITS];
       out[SAGA_C_MISSES] = s_ctr[SAGA_C_MISSES];
       out[SAGA_C_MIG_HITS] = s_ctr[SAGA_C_MIG_HITS];
@@ -1071,6 +1080,10 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       out[SAGA_C_VICTIM_HASH] = s_ctr[SAGA_C_VICTIM_HASH];
       out[SAGA_C_INFEASIBLE_EPOCH] = infeasible;
       out[SAGA_C_PEAK_RESIDENT] = c_peak;
+      out[SAGA_C_PF_HITS] = s_ctr[SAGA_C_PF_HITS];
+      out[SAGA_C_PF_MISSES] = s_ctr[SAGA_C_PF_MISSES];
+      out[SAGA_C_RESERVED18] = 0;
+      out[SAGA_C_RESERVED19] = 0;
       if (a.item_cyc) a.item_cyc[it] = (unsigned long long)(clock64() - t_start);
       if (a.phase_cyc)
         for (int i = 0; i < 8; ++i) a.phase_cyc[(uint64_t)it * 8 + i] = (unsigned long long)ph[i];
@@ -1151,7 +1164,8 @@ __global__ void k_unit_of(const uint32_t* hpos, uint64_t N, const uint32_t* u_ki
                           uint32_t* u_of) {
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t u = hpos[p + 1] - 1;
-    u_of[p] = u | (u_kind[u] ? KIND_MIG : 0u) | ((urec[u].lo & LO_SHARED) ? U_SHARED : 0u);
+    u_of[p] = u | (u_kind[u] == 1 ? KIND_MIG : 0u) | (u_kind[u] == 2 ? KIND_PF : 0u) |
+              ((urec[u].lo & LO_SHARED) ? U_SHARED : 0u);
   }
 }
 __global__ void k_ev_index(TraceView v, const uint64_t* ev_pos, const uint32_t* ev_e, uint32_t J, const uint32_t* hpos,
@@ -1171,13 +1185,7 @@ __global__ void k_ev_index(TraceView v, const uint64_t* ev_pos, const uint32_t* 
     upd_lo[i] = s2lo[v.call_sess[upd_c[i]]];
 }
 
-// previous occurrence of the block at each position (the inverse of next_use) and its unit
-__global__ void k_prev(const uint32_t* nxt, uint64_t N, uint32_t* prv) {
-  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t q = nxt[p];
-    if (q != INF32) prv[q] = (uint32_t)p;
-  }
-}
+// unit of the previous occurrence of the block at each position
 __global__ void k_prev_unit(const uint32_t* prv, const uint32_t* u_of, uint64_t N, uint32_t* upu) {
   for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t q = prv[p];
@@ -1207,14 +1215,9 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   SAGA_CK(cudaMemsetAsync(sflag, 0, (size_t(NS) + 1) * 4, s));
   nd.ev_pos = dalloc<uint64_t>(t, size_t(J) + 1);
   nd.u_of = dalloc<uint32_t>(t, N);
-  nd.prv = dalloc<uint32_t>(t, N);
   nd.upu = dalloc<uint32_t>(t, N);
-  if (!nd.ev_pos || !nd.u_of || !nd.prv || !nd.upu) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
-  SAGA_CK(cudaMemsetAsync(nd.prv, 0xFF, std::max<uint64_t>(N, 1) * 4, s));
-  if (N > 0) {
-    k_prev<<<grid_for(N), NTHREADS, 0, s>>>(nd.nxt, N, nd.prv);
-    count_launch();
-  }
+  if (!nd.ev_pos || !nd.u_of || !nd.upu) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
+  // nd.prv (previous occurrence of each position's block) comes from the segmented scan of A4
   k_ev_pos<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(nd.g_pos, nd.ev_g, J, nd.ev_pos);
   count_launch();
   if (nd.n_local) {
@@ -1233,6 +1236,7 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   SAGA_CK(d2h(&hv[1], s2lo + NS, 4, s));
   SAGA_CK(cudaStreamSynchronize(s));
   const uint32_t nu = hv[0];
+  if (nu >= (1u << 29)) { set_error("node %u has %u units (limit 2^29)", w, nu); return SAGA_ERR_STATE; }
   nd.n_units = nu;
   nd.n_lo = hv[1];
   nd.urec = dalloc<UnitRec>(t, nu);
@@ -1315,14 +1319,23 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
     x.urec = static_cast<const UnitRec*>(nd.urec); x.lid2gid = nd.lid2gid; x.upd_c = nd.upd_c; x.upd_lo = nd.upd_lo;
     hn[w] = x;
   }
-  // items, largest capacity first (the per-event cost grows with |S| <= C)
+  // items, longest first: by policy (measured per-event cost: AEG > LRU + Prefix > LRU > EVICT_ALL
+  // > BELADY), then largest capacity first (the per-event cost grows with |S| <= C).  Persistent
+  // CTAs take items in this order, so the long items start first and the short ones fill the
+  // tail (and a following launch on another stream can use the SMs the short ones free).
   std::vector<uint32_t> items;
   items.reserve(size_t(n_pol) * n_caps * n_owned);
   std::vector<uint32_t> corder(n_caps);
   for (uint32_t i = 0; i < n_caps; ++i) corder[i] = i;
   std::stable_sort(corder.begin(), corder.end(), [&](uint32_t x, uint32_t y) { return caps[x] > caps[y]; });
-  for (uint32_t ci : corder)
-    for (uint32_t pi = 0; pi < n_pol; ++pi)
+  std::vector<uint32_t> porder(n_pol);
+  for (uint32_t i = 0; i < n_pol; ++i) porder[i] = i;
+  auto prank = [](uint32_t p) {
+    return p == SAGA_POLICY_AEG ? 0 : p == SAGA_POLICY_LRU_PREFIX ? 1 : p == SAGA_POLICY_LRU ? 2 : p == SAGA_POLICY_EVICT_ALL ? 3 : 4;
+  };
+  std::stable_sort(porder.begin(), porder.end(), [&](uint32_t x, uint32_t y) { return prank(pol[x]) < prank(pol[y]); });
+  for (uint32_t pi : porder)
+    for (uint32_t ci : corder)
       for (uint32_t ni = 0; ni < n_owned; ++ni) items.push_back((pi << 28) | (ci << 12) | ni);
   const uint32_t n_items = (uint32_t)items.size();
 #if !SAGA_REPLAY_IS_WIDE
@@ -1409,6 +1422,11 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   SAGA_CK(ws_malloc((void**)&d_list, 4 * n_owned, s));
   SAGA_CK(ws_malloc((void**)&d_items, 4 * n_items, s));
   SAGA_CK(ws_malloc((void**)&work, 32, s));
+  if (!t->replay_status) {  // [0] error flag, [1..4] first failed invariant (checked by saga_replay_wait)
+    t->replay_status = dalloc<uint32_t>(t, 8);
+    if (!t->replay_status) { set_error("out of device memory (replay)"); return SAGA_ERR_OOM; }
+    SAGA_CK(cudaMemsetAsync(t->replay_status, 0, 32, s));
+  }
   if (trace) SAGA_CK(ws_malloc((void**)&d_cyc, 8ull * 9 * n_items, s));
   if (ws_malloc((void**)&scratch, a.cta_bytes * grid, s) != cudaSuccess) {
     set_error("out of device memory (replay scratch %llu bytes)", (unsigned long long)(a.cta_bytes * grid));
@@ -1426,7 +1444,7 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   a.alpha = cfg->alpha; a.beta = cfg->beta; a.gamma = cfg->gamma;
   a.p_low = cfg->p_low_pm; a.p_high = cfg->p_high_pm; a.ttl_max = cfg->ttl_max_us;
   a.callkey = static_cast<const CallKey*>(t->callkey);
-  a.scratch = scratch; a.work = work; a.err = work + 1; a.dbg = work + 4; a.item_cyc = d_cyc;
+  a.scratch = scratch; a.work = work; a.err = t->replay_status; a.dbg = t->replay_status + 4; a.item_cyc = d_cyc;
   a.phase_cyc = d_cyc ? d_cyc + n_items : nullptr;
   a.vlog = reinterpret_cast<unsigned long long*>(vlog);
   a.vlog_n = reinterpret_cast<unsigned long long*>(vlog_n);
@@ -1436,16 +1454,14 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   prof_end(SAGA_PROF_REPLAY, s);
   count_launch();
   SAGA_CK_LAUNCH();
-  uint32_t hw[8] = {0};
-  SAGA_CK(d2h(hw, work, 32, s));
-  const uint32_t& herr = hw[1];
+  // asynchronous: the scratch returns to the stream-ordered cache; the kernel's internal checks
+  // land in t->replay_status and are reported by saga_replay_wait (or a synchronising call)
   std::vector<unsigned long long> cyc(trace ? 9ull * n_items : 0);
   if (trace) SAGA_CK(d2h(cyc.data(), d_cyc, 8ull * 9 * n_items, s));
   ws_free(d_nodes, s); ws_free(d_caps, s); ws_free(d_list, s); ws_free(d_items, s);
   ws_free(scratch, s);
   ws_free(work, s);
   if (d_cyc) ws_free(d_cyc, s);
-  SAGA_CK(cudaStreamSynchronize(s));
   if (trace) {
     fprintf(stderr, "[saga replay] grid %u x %d threads, dyn smem %llu B (c1 %s, dead bits %s, ocall %s), %u items\n",
             grid, RT, (unsigned long long)dyn, a.dyn_c1 ? "smem" : "global", a.dyn_dbits_words ? "smem" : "global",
@@ -1459,11 +1475,22 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
               ph[0] / 1e6, ph[1] / 1e6, ph[2] / 1e6, ph[3] / 1e6, ph[4] / 1e6, ph[5] / 1e6, ph[6] / 1e6, ph[7] / 1e6);
     }
   }
-  if (herr || hw[4]) {
+  return SAGA_OK;
+}
+
+#if !SAGA_REPLAY_IS_WIDE
+// the kernel's internal checks of every replay launched so far on the handle (syncs its stream)
+saga_status replay_check(saga_trace* t) {
+  if (!t->replay_status) return SAGA_OK;
+  uint32_t hw[8] = {0};
+  SAGA_CK(d2h(hw, t->replay_status, 32, t->stream));
+  SAGA_CK(cudaStreamSynchronize(t->stream));
+  if (hw[0] || hw[4]) {
     set_error("saga_replay: internal selection check failed (k_replay.cu:%u values %u %u %u)", hw[4], hw[5], hw[6], hw[7]);
     return SAGA_ERR_STATE;
   }
   return SAGA_OK;
 }
+#endif
 
 }  // namespace saga

@@ -1,17 +1,21 @@
 // A5 / A6 in bulk (saga_aeg_score, saga_evict_select): the same key and selection device code
-// as the replay, over caller-provided candidate batches (one CTA per segment).
+// as the replay, over caller-provided candidate batches.
 //
-// Score: pass 1 max-reduces tau_max = max(T_e - t_last) and size_max over the segment
-// (eq:recency / eq:size normalisers); pass 2 evaluates eq:eviction in fp32 with the
-// pinned op order, quantises q = floor(score * 2^20) and the Alg. 1 / eq:pressure protection
-// bit, and writes key = (!prot << 63) | (q << 32) | lid.  A segment's candidate rows are read
-// twice; with one 1024-thread CTA per SM the second read hits L2 (<= 512 KB per segment).
+// Score (AEG): one CTA per segment.  Pass 1 max-reduces the eq:recency / eq:size normalisers
+// tau_max = max(T_e - t_last) and size_max over the segment; pass 2 evaluates
+// eq:eviction in fp32 with the pinned op order, quantises q = floor(score * 2^20) and the Alg. 1 /
+// eq:pressure protection bit, and writes key = (!prot << 63) | (q << 32) | lid.  The second read
+// of a segment's rows hits L2 (one 1024-thread CTA per SM keeps <= 148 x 384 KB in flight).
+// (A 4-CTA-cluster variant that staged the rows in shared memory and combined the normalisers
+// over DSMEM measured 0.44 ms vs 0.34 ms: cluster barriers dominated its stalls.)
 // Session state c*(s, e) = newest call of s admitted at or before e (binary search; each lane
 // caches its last owner because candidates arrive in runs of one session's blocks).
+// Score (BELADY): key = (nu << 32) | lid, a flat 128-bit streaming pass.
 //
 // Select: radix select of the k largest keys (block_select.cuh), then the k winners are
 // bitonic-sorted in descending order in a global scratch area and their segment-relative
-// indices written out.
+// indices written out.  (A 4-CTA-cluster variant staging the keys in shared memory measured
+// 0.32 ms vs 0.17 ms: cluster-barrier waits were half of its stall samples.)
 #include "block_select.cuh"
 
 namespace saga {
@@ -39,7 +43,7 @@ __device__ __forceinline__ uint32_t cstar(const TraceView& v, uint32_t s, uint32
   const uint32_t base = lo;
   while (lo < hi) {
     uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(&v.ecall[__ldg(&v.sc_call[mid])]) <= e) lo = mid + 1; else hi = mid;
+    if (__ldg(&v.sc_e[mid]) <= e) lo = mid + 1; else hi = mid;
   }
   return lo > base ? __ldg(&v.sc_call[lo - 1]) : 0u;
 }
@@ -143,6 +147,31 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+
+// BELADY keys (nu << 32) | lid over the whole candidate array: segments do not matter
+__global__ void __launch_bounds__(256) k_key_belady(const uint32_t* __restrict__ lid, const uint32_t* __restrict__ nu,
+                                                    const uint64_t* __restrict__ seg_off, uint32_t n_seg, bool vec,
+                                                    uint64_t* __restrict__ key) {
+  const uint64_t n = seg_off[n_seg], n0 = seg_off[0];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  if (vec) {  // 16-byte aligned: 4 candidates per thread and iteration
+    const uint64_t nq = (n - n0) / 4;
+    const uint4* l4 = reinterpret_cast<const uint4*>(lid + n0);
+    const uint4* u4 = reinterpret_cast<const uint4*>(nu + n0);
+    ulonglong2* k2 = reinterpret_cast<ulonglong2*>(key + n0);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += stride) {
+      const uint4 a = __ldcs(l4 + i), b = __ldcs(u4 + i);
+      __stcs(k2 + 2 * i, make_ulonglong2(((unsigned long long)b.x << 32) | a.x, ((unsigned long long)b.y << 32) | a.y));
+      __stcs(k2 + 2 * i + 1, make_ulonglong2(((unsigned long long)b.z << 32) | a.z, ((unsigned long long)b.w << 32) | a.w));
+    }
+    for (uint64_t i = n0 + nq * 4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+      key[i] = ((uint64_t)nu[i] << 32) | lid[i];
+  } else {
+    for (uint64_t i = n0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+      __stcs(&key[i], ((uint64_t)__ldcs(&nu[i]) << 32) | __ldcs(&lid[i]));
   }
 }
 
@@ -339,9 +368,13 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
   a.alpha = cfg->alpha; a.beta = cfg->beta; a.gamma = cfg->gamma;
   a.p_low = cfg->p_low_pm; a.p_high = cfg->p_high_pm; a.ttl_max = cfg->ttl_max_us;
   a.score = score; a.key = key;
-  const unsigned grid = std::min<unsigned>(b->n_seg, nsm_count());
   prof_begin(SAGA_PROF_SCORE, s);
-  k_score<<<grid, ST, 0, s>>>(a);
+  if (b->policy == SAGA_POLICY_BELADY) {
+    const bool vec = ((uintptr_t)b->cand_lid % 16 == 0) && ((uintptr_t)b->cand_nu % 16 == 0) && ((uintptr_t)key % 16 == 0);
+    k_key_belady<<<nsm_count() * 8, 256, 0, s>>>(b->cand_lid, b->cand_nu, b->seg_off, b->n_seg, vec, key);
+  } else {
+    k_score<<<std::min<unsigned>(b->n_seg, nsm_count()), ST, 0, s>>>(a);
+  }
   prof_end(SAGA_PROF_SCORE, s);
   count_launch();
   SAGA_CK_LAUNCH();

@@ -284,12 +284,17 @@ saga_status saga_load_trace_ex(const saga_trace_desc* desc, const saga_place_cfg
   t->n_sessions = desc->n_sessions;
   t->n_types = desc->n_types;
   t->n_nodes = desc->n_nodes;
+  t->load_flags = flags;
   saga_status st = load_validate_and_derive(t, desc);
   if (st != SAGA_OK) { saga_free_trace(t); return st; }
   t->owned_mask = owned_node_mask ? owned_node_mask : (desc->n_nodes >= 32 ? 0xFFFFFFFFu : ((1u << desc->n_nodes) - 1u));
   t->nodes.assign(desc->n_nodes, NodeDev());
   st = run_placement(t);
   if (st != SAGA_OK) { saga_free_trace(t); return st; }
+  if (flags & SAGA_LOAD_PREFETCH) {
+    st = run_prefetch_plan(t);
+    if (st != SAGA_OK) { saga_free_trace(t); return st; }
+  }
   for (uint32_t w = 0; w < desc->n_nodes; ++w) {
     if (!((t->owned_mask >> w) & 1u)) continue;
     t->nodes[w].owned = true;
@@ -387,6 +392,9 @@ saga_status saga_node_stream(const saga_trace* t, uint32_t node, uint32_t* block
   if (grp_t_dev && nd.G) SAGA_CK(cudaMemcpyAsync(grp_t_dev, nd.g_t, size_t(nd.G) * 8, cudaMemcpyDeviceToDevice, s));
   if (inv_dev && nd.n_inv) SAGA_CK(cudaMemcpyAsync(inv_dev, nd.inv_s, size_t(nd.n_inv) * 4, cudaMemcpyDeviceToDevice, s));
   SAGA_CK_LAUNCH();
+  // the handle's stream waits for these reads: saga_free_trace (which syncs it) cannot recycle
+  // the trace's buffers while the caller's stream still reads them
+  GUARD(const_cast<saga_trace*>(t), join(s, t->stream));
   return SAGA_OK;
 }
 
@@ -398,6 +406,22 @@ saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_us
   GUARD(t, join((cudaStream_t)stream, t->stream));
   GUARD(t, ensure_expanded(t, node));
   GUARD(t, run_next_use(t, node, next_use_dev, local_id_dev, t->stream));
+  GUARD(t, join(t->stream, (cudaStream_t)stream));
+  return SAGA_OK;
+}
+
+saga_status saga_belady_next_use_nodes(saga_trace* t, const uint32_t* nodes, uint32_t n_nodes, saga_stream_t stream) {
+  CHECK_HANDLE(t);
+  if (n_nodes && !nodes) { set_error("saga_belady_next_use_nodes: NULL argument"); return SAGA_ERR_INVALID_ARG; }
+  for (uint32_t i = 0; i < n_nodes; ++i)
+    if (nodes[i] >= t->n_nodes || !t->nodes[nodes[i]].owned) {
+      set_error("saga_belady_next_use_nodes: node %u not owned", nodes[i]);
+      return SAGA_ERR_STATE;
+    }
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(t, join((cudaStream_t)stream, t->stream));
+  for (uint32_t i = 0; i < n_nodes; ++i) GUARD(t, ensure_expanded(t, nodes[i]));
+  GUARD(t, run_next_use_nodes(t, nodes, n_nodes, t->stream));
   GUARD(t, join(t->stream, (cudaStream_t)stream));
   return SAGA_OK;
 }
@@ -429,6 +453,7 @@ saga_status saga_aeg_score(const saga_trace* t, const saga_score_batch* batch, c
   SAGA_CK(cudaSetDevice(t->device));
   GUARD(const_cast<saga_trace*>(t), join(t->stream, (cudaStream_t)stream));
   GUARD(const_cast<saga_trace*>(t), run_score(t, batch, cfg, score_dev, key_dev, stream ? (cudaStream_t)stream : t->stream));
+  GUARD(const_cast<saga_trace*>(t), join((cudaStream_t)stream, t->stream));  // see saga_node_stream
   return SAGA_OK;
 }
 
@@ -460,6 +485,7 @@ saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_d
   GUARD(const_cast<saga_trace*>(t), join(t->stream, s));
   GUARD(const_cast<saga_trace*>(t), run_pattern(t, call_label_dev, n_labels, session_role_dev, theta_pm, min_tasks,
                                                 counts_dev, tasks_dev, pred_dev, prob_dev, eval_dev, s));
+  GUARD(const_cast<saga_trace*>(t), join(s, t->stream));  // see saga_node_stream
   return SAGA_OK;
 }
 
@@ -480,6 +506,7 @@ saga_status saga_tool_stats(const saga_trace* t, const uint32_t* call_label_dev,
   GUARD(const_cast<saga_trace*>(t), join(t->stream, s));
   GUARD(const_cast<saga_trace*>(t), run_tool_stats(t, call_label_dev, n_labels, p_pm, window, min_samples, ema_terms,
                                                    ttl_out_dev, obs_out_dev, s));
+  GUARD(const_cast<saga_trace*>(t), join(s, t->stream));  // see saga_node_stream
   return SAGA_OK;
 }
 
@@ -503,6 +530,7 @@ saga_status saga_replay_victims(saga_trace* t, const saga_replay_cfg* cfg, uint3
   if (st == SAGA_OK) SAGA_CK(d2h(n_logged, cnt, 8, t->stream));
   ws_free(cnt, t->stream);
   GUARD(t, st);
+  GUARD(t, replay_check(t));
   GUARD(t, join(t->stream, (cudaStream_t)stream));
   return SAGA_OK;
 }
@@ -523,6 +551,13 @@ saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_
   GUARD(t, join((cudaStream_t)stream, t->stream));
   GUARD(t, run_replay(t, cfg, caps, n_caps, nodes, n_owned, counters_dev, t->stream));
   GUARD(t, join(t->stream, (cudaStream_t)stream));
+  return SAGA_OK;
+}
+
+saga_status saga_replay_wait(saga_trace* t) {
+  CHECK_HANDLE(t);
+  SAGA_CK(cudaSetDevice(t->device));
+  GUARD(t, replay_check(t));
   return SAGA_OK;
 }
 

@@ -93,9 +93,12 @@ struct TraceView {
   const uint32_t* fcall;   // [n_blocks] first call (global (t, s) order) touching the block, or NONE
   const uint32_t* sc_off;  // [n_sessions+1] calls of each session (CSR, ascending)
   const uint32_t* sc_call;
+  const uint32_t* sc_e;    // [n_calls] admission epoch of sc_call[i] (one load per binary-search step)
   const float* ci_P;       // P_reuse(s) after call c (eq:reuse + eq:overlap), fp32 pinned
   const uint32_t* ci_size; // size(s) after call c in blocks (eq:size numerator)
   const uint8_t* ci_fin;   // is_last or terminal
+  const uint32_t* pf_e = nullptr;    // [n_calls] PREFETCH boundary of the call (0 = none; SAGA_LOAD_PREFETCH)
+  const uint32_t* pf_len = nullptr;  // [n_calls] blocks of its predicted prefix
 };
 
 struct NodeDev {
@@ -123,6 +126,7 @@ struct NodeDev {
   uint32_t n_local = 0, w_lo = 0, w_hi = 0;
   uint32_t* lidf = nullptr;    // [N] local id | LID_FTN | LID_NFIE
   uint32_t* nxt = nullptr;     // [N] next use
+  uint32_t* prv = nullptr;     // [N] previous occurrence of the position's block (NONE at a first touch)
   uint32_t* lown = nullptr;    // [n_local] owner of the local block
   uint32_t* lid2gid = nullptr; // [n_local] global block id of the local block (ascending)
   uint32_t n_upd = 0;
@@ -135,7 +139,6 @@ struct NodeDev {
   uint32_t* ev_unit = nullptr; // [J+1] first unit of event j
   uint32_t* ev_upd = nullptr;  // [J] end of the session-update list for event j
   uint32_t* u_of = nullptr;    // [N] unit of position p | KIND_MIG
-  uint32_t* prv = nullptr;     // [N] previous position of the block at p (NONE at a first touch)
   uint32_t* upu = nullptr;     // [N] unit of prv[p]
   void* urec = nullptr;        // [n_units] UnitRec (k_replay.cu): t, position range, local owner
   uint32_t n_lo = 0;           // private owners (sessions) with blocks at this node
@@ -159,8 +162,10 @@ struct saga_trace {
   saga::ActRec* act = nullptr;      // [n_act]
   uint32_t n_mig = 0, n_act = 0;
   int64_t n_steals = 0, n_reroutes = 0;
+  uint32_t load_flags = 0;          // SAGA_LOAD_* of saga_load_trace_ex
   std::vector<saga::NodeDev> nodes;
   void* callkey = nullptr;          // [n_calls] CallKey (k_replay.cu), built by the first replay
+  uint32_t* replay_status = nullptr; // [8] the replay kernels' internal-check words (saga_replay_wait)
   std::vector<void*> allocs;        // every device allocation owned by the handle
 };
 
@@ -238,17 +243,19 @@ struct KeyCtx {
   float alpha, beta, gamma;
 };
 
-// eq:eviction / eq:recency / eq:size in fp32 with explicit round-to-nearest ops (no contraction)
-__device__ __forceinline__ float wa_lru_score(const KeyCtx& x, int64_t t_last, uint32_t size, float P) {
-  int64_t d = x.Te - t_last;
-  float R = x.tau > 0 ? fminf(1.0f, __fdiv_rn(__ll2float_rn(d), __ll2float_rn(x.tau))) : 0.0f;
+// eq:eviction / eq:recency / eq:size in fp32 with explicit round-to-nearest ops (no contraction);
+// fd = (float) (T_e - t_last), rounded to nearest (callers that stage candidates keep fd)
+__device__ __forceinline__ float wa_lru_score_fd(const KeyCtx& x, float fd, uint32_t size, float P) {
+  float R = x.tau > 0 ? fminf(1.0f, __fdiv_rn(fd, __ll2float_rn(x.tau))) : 0.0f;
   float S = __fdiv_rn(__ll2float_rn((long long)size), __ll2float_rn((long long)x.smax));
   float a = __fmul_rn(x.alpha, R);
   float b = __fmul_rn(x.beta, __fsub_rn(1.0f, P));
   float c = __fmul_rn(x.gamma, S);
   return __fadd_rn(__fadd_rn(a, b), c);
 }
-
+__device__ __forceinline__ float wa_lru_score(const KeyCtx& x, int64_t t_last, uint32_t size, float P) {
+  return wa_lru_score_fd(x, __ll2float_rn(x.Te - t_last), size, P);
+}
 __device__ __forceinline__ uint32_t quantize_q20(float s) {
   float f = floorf(__fmul_rn(s, 1048576.0f));
   if (!(f > 0.0f)) return 0u;  // also maps NaN to 0
@@ -280,8 +287,11 @@ cudaError_t scan_u32(saga_trace* t, const uint32_t* in, uint32_t* out, uint64_t 
 
 saga_status load_validate_and_derive(saga_trace* t, const saga_trace_desc* d);
 saga_status run_placement(saga_trace* t);
+saga_status run_prefetch_plan(saga_trace* t);
+saga_status replay_check(saga_trace* t);
 saga_status run_expand(saga_trace* t, uint32_t w);
 saga_status run_next_use(saga_trace* t, uint32_t w, uint32_t* next_use_out, uint32_t* lid_out, cudaStream_t s);
+saga_status run_next_use_nodes(saga_trace* t, const uint32_t* nodes, uint32_t n, cudaStream_t s);
 saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga_replay_cfg* cfg, float* score,
                       uint64_t* key, cudaStream_t s);
 saga_status run_select(const uint64_t* key, const uint64_t* seg_off, const uint32_t* k, uint32_t n_seg,
@@ -299,6 +309,15 @@ saga_status run_pattern(const saga_trace* t, const uint32_t* label, uint32_t n_l
 // radix sort of (key u32, value = position) pairs: sorted keys and values into *_out
 cudaError_t onesweep_sort_pairs(saga_trace* t, const uint32_t* keys_in, uint64_t n, uint32_t key_bits,
                                 uint32_t* keys_out, uint32_t* vals_out, cudaStream_t s);
+// the same over independent segments (one per cache node) in one launch per pass; keys_in /
+// keys_out / vals_out of every job 16-byte aligned
+struct SortJob {
+  const uint32_t* keys_in;
+  uint64_t n;
+  uint32_t* keys_out;
+  uint32_t* vals_out;
+};
+cudaError_t onesweep_sort_segments(saga_trace* t, const SortJob* jobs, uint32_t nseg, uint32_t key_bits, cudaStream_t s);
 
 }  // namespace saga
 

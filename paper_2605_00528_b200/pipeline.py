@@ -17,7 +17,7 @@ def owned_nodes(n_nodes: int, rank: int, world: int):
 
 def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, world: int = 1, comm=None,
              device: int = 0, stream=None, host=None, counters=None, shard_caps: bool = False,
-             before_expand=None, after_replay=None, mark=None):
+             before_expand=None, after_replay=None, mark=None, range_comm=None, replay_wait: bool = True):
     """Returns (trace handle, caps list, counters tensor [n_pol, n_caps, n_nodes, 16]).
 
     before_expand(stream), when given, defers A3 (SAGA_LOAD_DEFER_EXPAND) and is called between
@@ -35,17 +35,17 @@ def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, wo
                    stream=stream, host=host, defer_expand=before_expand is not None)
     if before_expand is not None:
         before_expand(t.stream)
-    for w in nodes:
-        t.next_use(w)
+    t.next_use_nodes(nodes)   # every owned node in one launch set per kernel (A4)
     if mark is not None:
         mark(t.stream, "nextuse")
     wlo, whi = 0, 0
     for w in nodes:
         a, b = t.sweep_range(w)
         wlo, whi = max(wlo, a), max(whi, b)
-    if comm is not None and world > 1:
+    rcomm = comm if (comm is not None and world > 1) else range_comm
+    if rcomm is not None:  # A8 #1 (range_comm: independent trials that still share one sweep)
         rng = torch.tensor([wlo, whi], dtype=torch.int64, device=f"cuda:{device}")
-        comm.allreduce(rng, op=1, stream=t.stream)
+        rcomm.allreduce(rng, op=1, stream=t.stream)
         t.stream.synchronize()
         wlo, whi = (int(x) for x in rng.cpu())
     caps = caps_fn(wlo, whi)
@@ -61,10 +61,10 @@ def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, wo
         mine = [i for i in range(len(caps)) if i % world == rank]
         for i in mine:
             sub = torch.zeros((npol, 1, desc.n_nodes, saga.NCOUNT), dtype=torch.int64, device=counters.device)
-            t.replay(replay_cfg, [caps[i]], nodes, sub)
+            t.replay(replay_cfg, [caps[i]], nodes, sub, wait=replay_wait)
             counters[:, i:i + 1].copy_(sub)
     elif nodes:
-        t.replay(replay_cfg, caps, nodes, counters)
+        t.replay(replay_cfg, caps, nodes, counters, wait=replay_wait)
     if mark is not None:
         mark(t.stream, "replay_q")
     if after_replay is not None:

@@ -15,10 +15,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libsaga.so")
 
 POLICY_AEG, POLICY_BELADY, POLICY_EVICT_ALL, POLICY_LRU, POLICY_LRU_PREFIX = 1, 2, 4, 8, 16
-NCOUNT = 16
+NCOUNT = 20
 COUNTERS = ["ACCESSES", "HITS", "MISSES", "COMPULSORY_GLOBAL", "COMPULSORY_NODE", "MIG_HITS", "MIG_MISSES",
             "INVALIDATED", "EVICTIONS", "EVICT_PROTECTED", "EVICT_EVENTS", "REGEN_TOKENS", "REGEN_US", "VICTIM_HASH",
-            "INFEASIBLE_EPOCH", "PEAK_RESIDENT"]
+            "INFEASIBLE_EPOCH", "PEAK_RESIDENT", "PF_HITS", "PF_MISSES", "RESERVED18", "RESERVED19"]
 CI = {n: i for i, n in enumerate(COUNTERS)}
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "TRACE", 3: "CAPACITY", 4: "STATE", 5: "OOM", 6: "CUDA", 7: "NCCL"}
 
@@ -79,6 +79,8 @@ def _load():
         "saga_node_stream_sizes": (i32, [vp, u32, C.POINTER(u64), C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
         "saga_node_stream": (i32, [vp, u32, vp, vp, vp, vp, vp, vp]),
         "saga_belady_next_use": (i32, [vp, u32, vp, vp, vp]),
+        "saga_belady_next_use_nodes": (i32, [vp, vp, u32, vp]),
+        "saga_replay_wait": (i32, [vp]),
         "saga_sweep_range": (i32, [vp, u32, C.POINTER(u32), C.POINTER(u32)]),
         "saga_aeg_score": (i32, [vp, C.POINTER(ScoreBatchC), C.POINTER(ReplayCfgC), vp, vp, vp]),
         "saga_evict_select": (i32, [vp, vp, vp, u32, vp, vp, vp]),
@@ -158,7 +160,7 @@ class Trace:
     """A loaded trace handle (saga_load_trace).  All methods are stream-ordered on `stream`."""
 
     def __init__(self, desc, place_cfg: dict, owned_mask: int = 0, device: int = 0, stream=None, host=None,
-                 defer_expand: bool = False):
+                 defer_expand: bool = False, prefetch: bool = False):
         import torch
         self.desc = desc
         self.device = device
@@ -167,7 +169,8 @@ class Trace:
         self._pc = place_cfg_c(place_cfg)
         h = C.c_void_p()
         _check(lib.saga_load_trace_ex(C.byref(self._host.c), C.byref(self._pc), owned_mask, device,
-                                      _stream_ptr(self.stream), 1 if defer_expand else 0, C.byref(h)))
+                                      _stream_ptr(self.stream), (1 if defer_expand else 0) | (2 if prefetch else 0),
+                                      C.byref(h)))
         self.h = h
 
     def free(self):
@@ -220,17 +223,29 @@ class Trace:
                                         local_id_out.data_ptr() if local_id_out is not None else None,
                                         _stream_ptr(self.stream)))
 
+    def next_use_nodes(self, nodes):
+        """A4 for several nodes in one launch set per kernel (saga_belady_next_use_nodes)."""
+        nodes = np.ascontiguousarray(nodes, np.uint32)
+        _check(lib.saga_belady_next_use_nodes(self.h, nodes.ctypes.data if nodes.size else None, nodes.size,
+                                              _stream_ptr(self.stream)))
+
     def sweep_range(self, node):
         a, b = C.c_uint32(), C.c_uint32()
         _check(lib.saga_sweep_range(self.h, node, C.byref(a), C.byref(b)))
         return a.value, b.value
 
-    def replay(self, rcfg: dict, caps, nodes, counters):
+    def replay(self, rcfg: dict, caps, nodes, counters, wait: bool = True):
+        """A7 (saga_replay, asynchronous); wait=True also runs saga_replay_wait (sync + checks)."""
         caps = np.ascontiguousarray(caps, np.uint32)
         nodes = np.ascontiguousarray(nodes, np.uint32)
         cfg = replay_cfg_c(rcfg)
         _check(lib.saga_replay(self.h, C.byref(cfg), caps.ctypes.data, caps.size, nodes.ctypes.data, nodes.size,
                                counters.data_ptr(), _stream_ptr(self.stream)))
+        if wait:
+            self.replay_wait()
+
+    def replay_wait(self):
+        _check(lib.saga_replay_wait(self.h))
 
     def pattern_infer(self, label, n_labels: int, role, theta_pm: int = 700, min_tasks: int = 30,
                       want_prob: bool = True, want_eval: bool = True):
@@ -255,7 +270,7 @@ class Trace:
         return out
 
     def replay_victims(self, rcfg: dict, cap: int, node: int, log_cap: int = 1 << 22):
-        """One (policy, cap, node) replay with its victim log.  Returns (counters int64[16] numpy,
+        """One (policy, cap, node) replay with its victim log.  Returns (counters int64[NCOUNT] numpy,
         victims uint64 numpy of (epoch << 32) | local id, epochs ascending)."""
         import torch
         cfg = replay_cfg_c(rcfg)

@@ -22,7 +22,7 @@ MUTATIONS = [
      "          for (size_t i = 0; i < cand.size(); ++i) {\n            float s32;",
      "          for (uint32_t b : S) x.smax = std::max(x.smax, owner_state(owner[nd.uniq[b]], e, ev.act).size);\n"
      "          for (size_t i = 0; i < cand.size(); ++i) {\n            float s32;"),
-    ("c* with e(c) < e instead of <=", "if (ecall[c] <= e) r = c;", "if (ecall[c] < e) r = c;"),
+    ("c* with e(c) < e instead of <=", "return ee < ecall[c]; });", "return ee <= ecall[c]; });"),
     ("n_cur = prompt only", "uint64_t ncur = uint64_t(prompt[c]) + outt[c];", "uint64_t ncur = uint64_t(prompt[c]);"),
     ("R and S swapped in eq:eviction", "((cfg.alpha * R) + (cfg.beta * (1.0f - st.P))) + (cfg.gamma * S)",
      "((cfg.alpha * S) + (cfg.beta * (1.0f - st.P))) + (cfg.gamma * R)"),

@@ -22,7 +22,7 @@ for it in range(3):
     t0 = time.perf_counter()
     lo = max(t.sweep_range(w)[0] for w in range(d.n_nodes)); hi = max(t.sweep_range(w)[1] for w in range(d.n_nodes))
     caps = sweep_caps(lo, hi, N_SWEEP.get("C2", 8), PHYSICAL_CAP.get("C2"))
-    ctr = torch.zeros((2, len(caps), d.n_nodes, 16), dtype=torch.int64, device="cuda")
+    ctr = torch.zeros((2, len(caps), d.n_nodes, saga.NCOUNT), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize(); T['sweep+alloc'] = time.perf_counter() - t0
     t0 = time.perf_counter()
     t.replay(dict(policy_mask=3), caps, list(range(d.n_nodes)), ctr)

@@ -57,21 +57,33 @@ def _properties(d, t, caps, ctr):
                 assert b[CI["MISSES"]] + b[CI["MIG_MISSES"]] == b[CI["COMPULSORY_NODE"]], (w, caps[c])
 
 
+def _next_use_all_nodes(d, t, o):
+    """next_use and local_id of every node, element by element, plus W_lo / W_hi and n_local."""
+    for w in range(d.n_nodes):
+        n, nl = t.info(w)
+        nu = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        lid = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        t.next_use(w, nu, lid)
+        torch.cuda.synchronize()
+        ref = o.next_use(w)
+        assert np.array_equal(nu.cpu().numpy().view(np.uint32)[:n], ref["next_use"]), w
+        assert np.array_equal(lid.cpu().numpy().view(np.uint32)[:n], ref["local_id"]), w
+        assert t.info(w)[1] == o.n_local(w) and t.sweep_range(w) == o.sweep_range(w), w
+        del nu, lid
+
+
 def test_c2_full_size_equals_oracle():
     d, pc, t, caps, ctr = _run("C2")
     o = O.Oracle(d, pc)
-    on, om, _, _ = o.placement()
-    gn, gm, _, _ = t.placement()
+    on, om, osteal, orr = o.placement()
+    gn, gm, gsteal, grr = t.placement()
     assert np.array_equal(on, gn)
-    assert np.array_equal(om, gm)
-    nu = torch.empty(t.info(0)[0], dtype=torch.int32, device="cuda")
-    t.next_use(0, nu, None)
-    torch.cuda.synchronize()
-    assert np.array_equal(nu.cpu().numpy().view(np.uint32), o.next_use(0)["next_use"])
+    assert np.array_equal(om, gm) and (osteal, orr) == (gsteal, grr)
+    _next_use_all_nodes(d, t, o)
     lo = max(o.sweep_range(w)[0] for w in range(d.n_nodes))
     hi = max(o.sweep_range(w)[1] for w in range(d.n_nodes))
     assert caps == sweep_caps(lo, hi, N_SWEEP["C2"], PHYSICAL_CAP.get("C2"))
-    idx = [0, len(caps) - 1]  # the tightest point and the physical capacity, every node
+    idx = [0, 2, 4, 6, len(caps) - 1]  # five of the nine sweep points, every node, both policies
     ref = o.replay_many(3, [caps[i] for i in idx])
     assert np.array_equal(ctr[:, idx], ref)
     _properties(d, t, caps, ctr)
@@ -79,11 +91,44 @@ def test_c2_full_size_equals_oracle():
 
 
 @pytest.mark.parametrize("name", ["C3", "C4"])
-def test_full_size_properties_and_sampled_node(name):
-    """C3 (288 items) and C4 (1,024 items) launch more items than SMs: the 256 x 2 replay shape."""
+def test_full_size_all_nodes(name):
+    """C3 (288 items) and C4 (1,024 items) launch more items than SMs: the 256 x 2 replay shape.
+    Every node at the tightest sweep point (and, for C3, the physical capacity) against the oracle."""
     d, pc, t, caps, ctr = _run(name)
     _properties(d, t, caps, ctr)
     o = O.Oracle(d, pc)
-    ref = o.replay_many(3, [caps[0]], nodes=[0])  # one node at the tightest capacity
-    assert np.array_equal(ctr[:, :1, 0], ref[:, :, 0])
+    on, om, _, _ = o.placement()
+    gn, gm, _, _ = t.placement()
+    assert np.array_equal(on, gn) and np.array_equal(om, gm)
+    idx = [0, len(caps) - 1] if name == "C3" else [0]
+    ref = o.replay_many(3, [caps[i] for i in idx])
+    assert np.array_equal(ctr[:, idx], ref)
+    if name == "C3":
+        _next_use_all_nodes(d, t, o)
+    t.free()
+
+
+def test_c5_full_size_sampled_nodes():
+    """C5 (100k sessions, 32 nodes, 2.9e9 accesses): placement of all 6.4 M calls, then nodes 0 and
+    1 (the only streams either side expands) at two capacities of the sweep, both policies."""
+    d = make("C5")
+    pc = place_cfg_for(d)
+    nodes = [0, 1]
+    t = saga.Trace(d, pc, owned_mask=0b11)
+    o = O.Oracle(d, pc, node_mask=0b11)
+    on, om, osteal, orr = o.placement()
+    gn, gm, gsteal, grr = t.placement()
+    assert np.array_equal(on, gn) and np.array_equal(om, gm) and (osteal, orr) == (gsteal, grr)
+    for w in nodes:
+        t.next_use(w)
+        assert t.sweep_range(w) == o.sweep_range(w), w
+    lo = max(o.sweep_range(w)[0] for w in nodes)
+    hi = max(o.sweep_range(w)[1] for w in nodes)
+    caps = sweep_caps(lo, hi, N_SWEEP["C5"], PHYSICAL_CAP.get("C5"))
+    sel = [caps[0], caps[4]]
+    got = torch.zeros((2, len(sel), d.n_nodes, saga.NCOUNT), dtype=torch.int64, device="cuda")
+    t.replay(dict(policy_mask=3), sel, nodes, got)
+    torch.cuda.synchronize()
+    ref = o.replay_many(3, sel, nodes=nodes)
+    assert np.array_equal(got.cpu().numpy()[:, :, nodes], ref[:, :, nodes])
     t.free()

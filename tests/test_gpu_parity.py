@@ -49,6 +49,19 @@ def small_cases():
     pc = place_cfg_for(d)
     pc.update(kappa=2)
     cases.append(("C5_32n_hot", d, pc))
+    # F4 speculative prefetch records (SAGA_LOAD_PREFETCH) on top of queues, steals and reroutes
+    for name, seed in (("rand1", 1), ("rand4", 4)):
+        d = make_random_small(seed, n_sessions=8, n_nodes=3, max_calls=5, max_blocks=8)
+        pc = default_place_cfg(seed)
+        if seed % 2:
+            pc.update(kappa=1, theta_pm=100000)
+        cases.append((name + "_pf", d, pc, True))
+    d = make("C2", n_sessions=40, n_nodes=4)
+    cases.append(("C2_pf", d, place_cfg_for(d), True))
+    d = make("C5", n_sessions=160, n_nodes=32)
+    pc = place_cfg_for(d)
+    pc.update(kappa=2)
+    cases.append(("C5_32n_hot_pf", d, pc, True))
     return cases
 
 
@@ -58,11 +71,11 @@ IDS = [c[0] for c in CASES]
 
 @pytest.fixture(scope="module", params=range(len(CASES)), ids=IDS)
 def pair(request):
-    name, d, pc = CASES[request.param]
-    o = O.Oracle(d, pc)
-    t = saga.Trace(d, pc)
-    for w in range(d.n_nodes):
-        t.next_use(w)
+    name, d, pc = CASES[request.param][:3]
+    pf = len(CASES[request.param]) > 3 and CASES[request.param][3]
+    o = O.Oracle(d, pc, prefetch=pf)
+    t = saga.Trace(d, pc, prefetch=pf)
+    t.next_use_nodes(list(range(d.n_nodes)))
     return name, d, pc, o, t
 
 
@@ -123,7 +136,7 @@ def test_replay_counters_equal(pair, variant, monkeypatch):
     caps = _caps_for(o, d, name)
     # AEG, BELADY, EVICT_ALL and the tab:competitive baselines LRU, LRU + Prefix
     ref = o.replay_many(31, caps)
-    got = torch.zeros((5, len(caps), d.n_nodes, 16), dtype=torch.int64, device="cuda")
+    got = torch.zeros((5, len(caps), d.n_nodes, saga.NCOUNT), dtype=torch.int64, device="cuda")
     t.replay(dict(policy_mask=31), caps, list(range(d.n_nodes)), got)
     torch.cuda.synchronize()
     g = got.cpu().numpy()
@@ -136,7 +149,7 @@ def test_replay_counters_equal(pair, variant, monkeypatch):
 def test_replay_deterministic(pair):
     name, d, pc, o, t = pair
     caps = _caps_for(o, d, name)[:2]
-    a = torch.zeros((2, len(caps), d.n_nodes, 16), dtype=torch.int64, device="cuda")
+    a = torch.zeros((2, len(caps), d.n_nodes, saga.NCOUNT), dtype=torch.int64, device="cuda")
     b = torch.zeros_like(a)
     t.replay(dict(policy_mask=3), caps, list(range(d.n_nodes)), a)
     t.replay(dict(policy_mask=3), caps, list(range(d.n_nodes)), b)
@@ -286,7 +299,7 @@ def test_state_errors():
     with pytest.raises(saga.SagaError) as ex:
         t.sweep_range(0)
     assert ex.value.status == 4
-    c = torch.zeros((1, 1, 1, 16), dtype=torch.int64, device="cuda")
+    c = torch.zeros((1, 1, 1, saga.NCOUNT), dtype=torch.int64, device="cuda")
     with pytest.raises(saga.SagaError):
         t.replay(dict(policy_mask=1), [10], [0], c)
     t.next_use(0)

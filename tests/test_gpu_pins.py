@@ -7,6 +7,7 @@ import pytest
 from gen import default_place_cfg
 from tests import test_oracle_keys as K
 from tests import test_oracle_place as PL
+from tests import test_oracle_prefetch as PF
 
 pytestmark = pytest.mark.gpu
 
@@ -112,3 +113,21 @@ def test_reroute_reprefill_is_regeneration_on_gpu():
         assert (n1[CI["MISSES"]], n1[CI["COMPULSORY_GLOBAL"]], n1[CI["COMPULSORY_NODE"]]) == (2, 1, 2)
         assert (n1[CI["REGEN_TOKENS"]], n1[CI["REGEN_US"]]) == (16, 3200)
         assert (n0[CI["MISSES"]], n0[CI["COMPULSORY_GLOBAL"]], n0[CI["REGEN_TOKENS"]]) == (2, 2, 0)
+
+
+def test_prefetch_hand_counts_on_gpu():
+    """tests/test_oracle_prefetch.py::test_prefetch_replay_evict_all_hand_counts on the GPU path."""
+    CI = saga.CI
+    for pf, want in ((True, dict(ACCESSES=17, HITS=4, MISSES=9, PF_HITS=0, PF_MISSES=4, COMPULSORY_GLOBAL=9,
+                                 REGEN_TOKENS=0, EVICTIONS=8)),
+                     (False, dict(MISSES=13, REGEN_TOKENS=64, PF_MISSES=0))):
+        t = saga.Trace(PF._replay_trace(), default_place_cfg(), prefetch=pf)
+        t.next_use(0)
+        got = torch.zeros((1, 1, 1, saga.NCOUNT), dtype=torch.int64, device="cuda")
+        t.replay(dict(policy_mask=saga.POLICY_EVICT_ALL), [100], [0], got)
+        torch.cuda.synchronize()
+        g = got.cpu().numpy()[0, 0, 0]
+        assert {k: int(g[CI[k]]) for k in want} == want, pf
+    s = saga.Trace(PF._replay_trace(), default_place_cfg(), prefetch=True).node_stream(0)
+    assert list(s["block"]) == [0, 1, 2, 3, 10, 11, 12, 13, 0, 1, 2, 3, 0, 1, 2, 3, 4]
+    assert [int(k) for k in s["groups"][:, 1]] == [0, 0, 2, 0]

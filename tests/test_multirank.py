@@ -48,7 +48,7 @@ def _worker(rank, world, port, kind, out_path):
         rng = torch.tensor([lo, hi], dtype=torch.int64)
         dist.all_reduce(rng, op=dist.ReduceOp.MAX)          # A8 #1
         caps = sweep_caps(int(rng[0]), int(rng[1]), 5)
-        ctr = np.zeros((3, len(caps), d.n_nodes, 16), dtype=np.int64)
+        ctr = np.zeros((3, len(caps), d.n_nodes, O.NCOUNT), dtype=np.int64)
         if shard_caps:
             mine = [i for i in range(len(caps)) if i % world == rank]
             for i in mine:

@@ -30,11 +30,11 @@ def O(oracle_lib):
 
 
 def misses(ctr, O):
-    return int(ctr[O.CI["MISSES"]] + ctr[O.CI["MIG_MISSES"]])
+    return int(ctr[O.CI["MISSES"]] + ctr[O.CI["MIG_MISSES"]] + ctr[O.CI["PF_MISSES"]])
 
 
 def hits(ctr, O):
-    return int(ctr[O.CI["HITS"]] + ctr[O.CI["MIG_HITS"]])
+    return int(ctr[O.CI["HITS"]] + ctr[O.CI["MIG_HITS"]] + ctr[O.CI["PF_HITS"]])
 
 
 # ------------------------------------------------------------------------------------------
