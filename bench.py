@@ -114,18 +114,33 @@ def sweep_for(name):
     return lambda lo, hi: sweep_caps(lo, hi, N_SWEEP.get(base, 8), PHYSICAL_CAP.get(base))
 
 
-def algorithmic_bytes(cat, n_access, n_replay_access, n_calls, key_bits):
-    """Algorithmic HBM bytes per step of each kernel family (DESIGN.md §7 "Roofline")."""
+def replay_bytes_per_access(policy_mask):
+    """Algorithmic bytes per access-replay of the replay kernel (12 fused / 20
+    unfused): the per-position words it streams for each record -- local id|flags, unit|kind and
+    next use (12 B, BELADY); AEG / EVICT_ALL / LRU also read the previous occurrence and its unit
+    (20 B).  Averaged over the policies of the mask (each policy replays every access once)."""
+    pols = [b for b in (1, 2, 4, 8, 16) if policy_mask & b]
+    return sum(12 if b == 2 else 20 for b in pols) / max(1, len(pols))
+
+
+def algorithmic_bytes(cat, n_access, n_replay_access, n_calls, key_bits, policy_mask=3):
+    """Algorithmic HBM bytes per step of each kernel family (DESIGN.md §6 "Kernels, rooflines")."""
     passes = max(1, (key_bits + 7) // 8)
     return {
         "sort": n_access * (4 + 12 + 16 * (passes - 1)),     # histogram read + pass 1 + later passes
-        "segscan": n_access * 16,                            # sorted (key, pos) read + next_use/lid writes
-        "epoch_stats": n_access * 8,                          # next_use + lid read in stream order
-        "replay": n_replay_access * 8,                        # per access-replay: lid|flags + next_use
+        "segscan": n_access * 20,                            # sorted (key, pos) read + next/prev/lid scattered
+        "epoch_stats": n_access * 16,                         # next, prev, lid read + lid|flags written
+        "replay": n_replay_access * replay_bytes_per_access(policy_mask),
         "expand": n_access * 4,                               # stream write
         "place": n_calls * 40,
         "load": n_calls * 40,
     }.get(cat, 0)
+
+
+def input_bytes_per_launch(cat, n_access):
+    """Bytes a launch of the kernel family reads as its main input (compared with the L2 size)."""
+    return {"sort": n_access * 8, "segscan": n_access * 8, "epoch_stats": n_access * 12, "expand": n_access * 4,
+            "replay": n_access * 20}.get(cat)
 
 
 def bulk_score_select(t, desc, stream, dev, reps=5, n_seg=1024, seg_len=32768, k_frac=0.01):
@@ -318,9 +333,20 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(desc, pc, caps, nthreads):
     """Oracle timed on a bounded sample: full oracle build (placement, streams) + next use of every
-    node + one replay per (node, policy) at the middle capacity."""
+    node + one replay per (node, policy) at the middle capacity, on every host thread; then node 0's
+    two replays again on ONE thread (the per-core rate)."""
     from oracle import oracle as O
     O.build()
     t0 = time.perf_counter()
@@ -329,9 +355,15 @@ def cpu_baseline(desc, pc, caps, nthreads):
     ctr = o.replay_many(3, cap, nthreads=nthreads)
     dt = time.perf_counter() - t0
     reps = int(ctr[:, :, :, 0].sum())
-    return {"value": reps / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+    t1 = time.perf_counter()
+    c1 = o.replay_many(3, cap, nodes=[0], nthreads=1)
+    dt1 = time.perf_counter() - t1
+    reps1 = int(c1[:, :, 0, 0].sum())
+    return {"value": reps / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{desc.name}: oracle build + all {desc.n_nodes} nodes x AEG+BELADY at capacity {cap[0]} "
-                      f"({reps} access-replays in {dt:.1f} s)"}
+                      f"({reps} access-replays in {dt:.1f} s)",
+            "single_thread": {"value": reps1 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"node 0 x AEG+BELADY at capacity {cap[0]} ({reps1} access-replays in {dt1:.1f} s)"}}
 
 
 def main():
@@ -604,34 +636,43 @@ def main():
 
     # ---- roofline of the dominant kernel family (per-launch, CUDA events on the launching stream) ----
     peak, peak_kind = hbm_peak()
+    l2_bytes = int(getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 0)) or None  # cudaDevAttrL2CacheSize
+    ncu_cfg = {}
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):  # ncu dram__bytes_read + write per launch, by config and kernel family
+        try:
+            ncu_cfg = json.load(open(tfile)).get(args.config, {}) if args.policy_mask == 3 else {}
+        except Exception:
+            ncu_cfg = {}
     key_bits = int(np.ceil(np.log2(max(desc.n_blocks, 2))))
     kernels = {}
     for i, nm in enumerate(PROF_NAMES):
         if pn[i] == 0:
             continue
         ms_k = pm[i] / prof_steps
-        byt = algorithmic_bytes(nm, n_access / max(world, 1) if not shard_caps else n_access,
-                                replay_accesses / max(world, 1), desc.n_calls, key_bits)  # per rank
+        n_loc = n_access / max(world, 1) if not shard_caps else n_access
+        byt = algorithmic_bytes(nm, n_loc, replay_accesses / max(world, 1), desc.n_calls, key_bits,
+                                args.policy_mask)  # per rank
+        ib = input_bytes_per_launch(nm, n_loc)
         kernels[nm] = {"ms_per_step": ms_k, "launches_per_step": pn[i] / prof_steps, "share": ms_k / ms_prof,
-                       "algorithmic_gb_s": (byt / (ms_k / 1e3) / 1e9) if byt and ms_k > 0 else None}
+                       "algorithmic_gb_s": (byt / (ms_k / 1e3) / 1e9) if byt and ms_k > 0 else None,
+                       "algorithmic_bytes_per_step": byt or None,
+                       "input_over_l2": (ib / l2_bytes) if ib and l2_bytes else None}
+        tr = ncu_cfg.get(nm)
+        if tr and byt:
+            kernels[nm]["ncu_dram_bytes_per_step"] = tr * pn[i] / prof_steps
+            kernels[nm]["traffic_over_algorithmic"] = tr * (pn[i] / prof_steps) / byt
     dom = max((k for k in kernels if k in ("sort", "segscan", "epoch_stats", "replay", "expand")),
               key=lambda k: kernels[k]["ms_per_step"], default=None)
-    traffic = None
-    tinfo = {}
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if dom and os.path.exists(tfile):
-        try:
-            tinfo = json.load(open(tfile))
-            traffic = tinfo.get(dom)
-        except Exception:
-            traffic = None
+    traffic = ncu_cfg.get(dom) if dom else None
+    tinfo = ncu_cfg
     roof = None
     if dom:
         ach = kernels[dom]["algorithmic_gb_s"] or 0.0
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "peak_source": peak_kind,
                 "note": "achieved = algorithmic bytes of the kernel family / its CUDA-event time per step"}
-        inst = tinfo.get(dom + "_warp_inst") if args.config == "C2" and args.policy_mask == 3 else None
+        inst = tinfo.get(dom + "_warp_inst")
         if inst:
             # the replay is issue/latency-bound: its warp-instruction rate against the SM issue peak
             # (148 SMs x 4 schedulers x 1 instruction per clock at the sampled SM clock), DESIGN.md §6
@@ -671,7 +712,9 @@ def main():
                                                                   (16, "LRU_PREFIX")) if args.policy_mask & b],
                        "trace_accesses": n_access, "access_replays_per_step": replay_accesses,
                        "trace_accesses_per_s": n_access / (ms / 1e3),
-                       "l2": "inputs larger than L2 (node streams 4 B/access + per-node next-use arrays)",
+                       "l2_bytes": l2_bytes,
+                       "l2": ("L2 not flushed between steps: every step loads a new trace and its per-access inputs "
+                              "exceed L2 (kernels.*.input_over_l2 = main input bytes of one launch / L2 size)"),
                        "steps_in_flight": inflight, "overlap": overlap, "step_latency_ms": lat_ms,
                        "sharding": ("independent trials (seed + 1000 r), counters all-reduced" if trials and world > 1
                                     else ("capacity points" if shard_caps else "cache nodes w mod R"))},

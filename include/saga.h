@@ -44,7 +44,7 @@ typedef enum {
   SAGA_OK = 0,
   SAGA_ERR_INVALID_ARG = 1, /* bad pointer / size / option; nothing was modified            */
   SAGA_ERR_TRACE = 2,       /* trace failed validation (message says which rule); outputs untouched */
-  SAGA_ERR_CAPACITY = 3,    /* a capacity is 0 (S:209 CapacityError); see saga_replay           */
+  SAGA_ERR_CAPACITY = 3,    /* a capacity below a single call's block count (S:209 CapacityError) */
   SAGA_ERR_STATE = 4,       /* call order violated (e.g. replay before next-use) or internal limit */
   SAGA_ERR_OOM = 5,         /* device allocation failed                                        */
   SAGA_ERR_CUDA = 6,        /* CUDA runtime error (sticky)                                     */
@@ -271,7 +271,8 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
  * the order AEG, BELADY, EVICT_ALL, LRU, LRU_PREFIX; cells of nodes not listed are left untouched (zero them
  * first; then an all-reduce sum over ranks is an exact gather).  A capacity below a node's
  * W_lo is data, not an error: INFEASIBLE_EPOCH is set and that replay stops counting.
- * SAGA_ERR_CAPACITY if a capacity is 0.  Stream-ordered and asynchronous once the node's replay
+ * SAGA_ERR_CAPACITY if a capacity is below the block count of a single call (or
+ * migration / prefetch group) at a replayed node (S:209 CapacityError).  Stream-ordered and asynchronous once the node's replay
  * index exists (the first call for a node builds it and syncs for its sizes); the kernel's
  * internal invariant checks are reported by saga_replay_wait.  Set SAGA_REPLAY_TRACE=1 to print
  * per-item / per-phase SM cycles to stderr (syncs). */

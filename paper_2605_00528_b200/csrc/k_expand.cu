@@ -60,7 +60,8 @@ __device__ __forceinline__ uint32_t count_le(const uint32_t* list, uint32_t n, c
 }
 __global__ void k_groups(TraceView v, const uint32_t* clist, uint32_t nC, const Mig* migs, const uint32_t* mlist,
                          uint32_t nM, const uint32_t* mig_e, const uint32_t* plist, uint32_t nP, uint32_t* g_call,
-                         uint32_t* g_kind, uint32_t* g_e, int64_t* g_t, uint64_t* g_len) {
+                         uint32_t* g_kind, uint32_t* g_e, int64_t* g_t, uint64_t* g_len,
+                         unsigned long long* max_len) {
   const uint32_t n = nC + nM + nP;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t dst, call, kind, e;
@@ -96,6 +97,7 @@ __global__ void k_groups(TraceView v, const uint32_t* clist, uint32_t nC, const 
     g_e[dst] = e;
     g_t[dst] = tv;
     g_len[dst] = len;
+    atomicMax(max_len, (unsigned long long)len);  // largest single-call block set (SAGA_ERR_CAPACITY)
   }
 }
 // epoch of each migration (key table for the merge ranks)
@@ -262,13 +264,16 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
   nd.g_pos = dalloc<uint64_t>(t, size_t(G) + 1);
   uint32_t* head = dalloc<uint32_t>(t, G);
   uint32_t* hpos = dalloc<uint32_t>(t, size_t(G) + 1);
+  unsigned long long* gmax = dalloc<unsigned long long>(t, 1);
+  if (!gmax) { set_error("out of device memory (expand)"); return SAGA_ERR_OOM; }
+  SAGA_CK(cudaMemsetAsync(gmax, 0, 8, s));
   if (!nd.g_call || !nd.g_kind || !nd.g_e || !nd.g_t || !g_len || !nd.g_pos || !head || !hpos) {
     set_error("out of device memory (expand)");
     return SAGA_ERR_OOM;
   }
   if (G > 0) {
     k_groups<<<grid_for(G), NTHREADS, 0, s>>>(v, clist, nC, t->migs, mlist, nM, mig_e, plist, nP, nd.g_call, nd.g_kind,
-                                              nd.g_e, nd.g_t, g_len);
+                                              nd.g_e, nd.g_t, g_len, gmax);
     k_ev_head<<<grid_for(G), NTHREADS, 0, s>>>(nd.g_e, G, head);
     count_launch(2);
   }
@@ -279,6 +284,9 @@ saga_status run_expand(saga_trace* t, uint32_t w) {
   SAGA_CK_LAUNCH();
   SAGA_CK(d2h(&Jr, hpos + G, 4, s));
   SAGA_CK(d2h(&N, nd.g_pos + G, 8, s));
+  unsigned long long gm = 0;
+  SAGA_CK(d2h(&gm, gmax, 8, s));
+  nd.max_group = gm;
   SAGA_CK(cudaStreamSynchronize(s));
   if (N >= (1ull << 31)) { set_error("node %u stream has %llu accesses (limit 2^31)", w, (unsigned long long)N); return SAGA_ERR_STATE; }
   nd.N = N;

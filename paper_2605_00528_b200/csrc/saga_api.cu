@@ -261,6 +261,7 @@ saga_status saga_load_trace(const saga_trace_desc* desc, const saga_place_cfg* c
 
 saga_status saga_load_trace_ex(const saga_trace_desc* desc, const saga_place_cfg* cfg, uint32_t owned_node_mask,
                                int device, saga_stream_t stream, uint32_t flags, saga_trace** out) {
+  SAGA_NVTX();
   g_err.clear();
   if (!desc || !cfg || !out) { set_error("saga_load_trace: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   *out = nullptr;
@@ -325,6 +326,7 @@ saga_status saga_trace_info(const saga_trace* t, uint32_t node, uint64_t* n_acce
 }
 
 saga_status saga_placement(const saga_trace* t, uint8_t* node_host, uint32_t* mig_host, uint64_t mig_cap, int64_t* stats) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   SAGA_CK(cudaSetDevice(t->device));
   if (node_host) SAGA_CK(d2h(node_host, t->node_of, t->n_calls, t->stream));
@@ -380,6 +382,7 @@ __global__ void k_pack_grp(const uint64_t* g_pos, const uint32_t* g_kind, uint32
 
 saga_status saga_node_stream(const saga_trace* t, uint32_t node, uint32_t* block_dev, uint32_t* ev_dev, uint64_t* grp_dev,
                              int64_t* grp_t_dev, uint32_t* inv_dev, saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("node %u not owned", node); return SAGA_ERR_STATE; }
   SAGA_CK(cudaSetDevice(t->device));
@@ -400,6 +403,7 @@ saga_status saga_node_stream(const saga_trace* t, uint32_t node, uint32_t* block
 
 saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_use_dev, uint32_t* local_id_dev,
                                  saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_belady_next_use: node %u not owned", node); return SAGA_ERR_STATE; }
   SAGA_CK(cudaSetDevice(t->device));
@@ -411,6 +415,7 @@ saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_us
 }
 
 saga_status saga_belady_next_use_nodes(saga_trace* t, const uint32_t* nodes, uint32_t n_nodes, saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if (n_nodes && !nodes) { set_error("saga_belady_next_use_nodes: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   for (uint32_t i = 0; i < n_nodes; ++i)
@@ -438,6 +443,7 @@ saga_status saga_sweep_range(const saga_trace* t, uint32_t node, uint32_t* w_lo,
 
 saga_status saga_aeg_score(const saga_trace* t, const saga_score_batch* batch, const saga_replay_cfg* cfg, float* score_dev,
                            uint64_t* key_dev, saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if (!batch || !cfg || !key_dev) { set_error("saga_aeg_score: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   if (batch->policy != SAGA_POLICY_AEG && batch->policy != SAGA_POLICY_BELADY) {
@@ -459,6 +465,7 @@ saga_status saga_aeg_score(const saga_trace* t, const saga_score_batch* batch, c
 
 saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_dev, const uint32_t* k_dev, uint32_t n_seg,
                               const uint64_t* out_off_dev, uint32_t* victim_idx_dev, saga_stream_t stream) {
+  SAGA_NVTX();
   g_err.clear();
   if (n_seg && (!key_dev || !seg_off_dev || !k_dev || !out_off_dev || !victim_idx_dev)) {
     set_error("saga_evict_select: NULL argument");
@@ -471,6 +478,7 @@ saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_d
                                const uint8_t* session_role_dev, uint32_t theta_pm, uint32_t min_tasks,
                                uint64_t* counts_dev, uint32_t* tasks_dev, uint32_t* pred_dev, float* prob_dev,
                                uint64_t* eval_dev, saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if ((t->n_calls && !call_label_dev) || (t->n_sessions && !session_role_dev) || !counts_dev || !tasks_dev || !pred_dev) {
     set_error("saga_pattern_infer: NULL argument");
@@ -492,6 +500,7 @@ saga_status saga_pattern_infer(const saga_trace* t, const uint32_t* call_label_d
 saga_status saga_tool_stats(const saga_trace* t, const uint32_t* call_label_dev, uint32_t n_labels, uint32_t p_pm,
                             uint32_t window, uint32_t min_samples, uint32_t ema_terms, int64_t* ttl_out_dev,
                             uint32_t* obs_out_dev, saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if ((t->n_calls && (!call_label_dev || !ttl_out_dev || !obs_out_dev))) {
     set_error("saga_tool_stats: NULL argument");
@@ -513,6 +522,7 @@ saga_status saga_tool_stats(const saga_trace* t, const uint32_t* call_label_dev,
 saga_status saga_replay_victims(saga_trace* t, const saga_replay_cfg* cfg, uint32_t cap, uint32_t node,
                                 uint64_t* log_dev, uint64_t log_cap, uint64_t* n_logged, int64_t* counters_dev,
                                 saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if (!cfg || !counters_dev || !n_logged || (log_cap && !log_dev)) { set_error("saga_replay_victims: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   const uint32_t pm = cfg->policy_mask & 31u;
@@ -521,6 +531,11 @@ saga_status saga_replay_victims(saga_trace* t, const saga_replay_cfg* cfg, uint3
   if (cap == 0 || cap > (1u << 28)) { set_error("saga_replay_victims: capacity %u out of range (1..2^28)", cap); return SAGA_ERR_CAPACITY; }
   if (node >= t->n_nodes || !t->nodes[node].owned) { set_error("saga_replay_victims: node %u not owned", node); return SAGA_ERR_STATE; }
   if (!t->nodes[node].nu_done) { set_error("saga_replay_victims: saga_belady_next_use(node %u) must run first", node); return SAGA_ERR_STATE; }
+  if (cap < t->nodes[node].max_group) {
+    set_error("saga_replay_victims: capacity %u is below the %llu blocks of a single call", cap,
+              (unsigned long long)t->nodes[node].max_group);
+    return SAGA_ERR_CAPACITY;
+  }
   SAGA_CK(cudaSetDevice(t->device));
   GUARD(t, join((cudaStream_t)stream, t->stream));
   uint64_t* cnt = nullptr;
@@ -537,6 +552,7 @@ saga_status saga_replay_victims(saga_trace* t, const saga_replay_cfg* cfg, uint3
 
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   if (!cfg || (n_caps && !caps) || (n_owned && !nodes) || !counters_dev) { set_error("saga_replay: NULL argument"); return SAGA_ERR_INVALID_ARG; }
   if ((cfg->policy_mask & ~31u) || !(cfg->policy_mask & 31u)) { set_error("saga_replay: bad policy_mask"); return SAGA_ERR_INVALID_ARG; }
@@ -546,6 +562,12 @@ saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_
   for (uint32_t i = 0; i < n_owned; ++i) {
     if (nodes[i] >= t->n_nodes || !t->nodes[nodes[i]].owned) { set_error("saga_replay: node %u not owned", nodes[i]); return SAGA_ERR_STATE; }
     if (!t->nodes[nodes[i]].nu_done) { set_error("saga_replay: saga_belady_next_use(node %u) must run first", nodes[i]); return SAGA_ERR_STATE; }
+    for (uint32_t c = 0; c < n_caps; ++c)
+      if (caps[c] < t->nodes[nodes[i]].max_group) {  // SPEC CapacityError: one call does not fit
+        set_error("saga_replay: capacity %u is below the %llu blocks of a single call at node %u", caps[c],
+                  (unsigned long long)t->nodes[nodes[i]].max_group, nodes[i]);
+        return SAGA_ERR_CAPACITY;
+      }
   }
   SAGA_CK(cudaSetDevice(t->device));
   GUARD(t, join((cudaStream_t)stream, t->stream));
@@ -555,6 +577,7 @@ saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_
 }
 
 saga_status saga_replay_wait(saga_trace* t) {
+  SAGA_NVTX();
   CHECK_HANDLE(t);
   SAGA_CK(cudaSetDevice(t->device));
   GUARD(t, replay_check(t));

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "saga.h"
 
 namespace saga {
@@ -50,6 +52,13 @@ struct ProfScope {
   ProfScope(int c, cudaStream_t st) : cat(c), s(st) { prof_begin(cat, s); }
   ~ProfScope() { prof_end(cat, s); }
 };
+// NVTX range over a host-side scope (ABI entry points): visible in Nsight timelines (header-only
+// NVTX3; no cost without an attached tool)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+#define SAGA_NVTX() saga::NvtxScope _saga_nvtx(__func__)
 
 struct Mig { uint32_t e, s, v, t; };
 struct ActRec { uint32_t e, w, mask, pad; };
@@ -108,6 +117,7 @@ struct NodeDev {
   uint32_t J = 0;          // events incl. the trailing sentinel
   uint32_t G = 0;          // record groups
   uint32_t n_inv = 0;
+  uint64_t max_group = 0;      // largest block set one call brings to the node (CALL / MIG / PREFETCH group)
   uint32_t* block = nullptr;
   uint32_t* ftg = nullptr;     // [N/32+1] bit p: CALL record p is its block's global first touch
   uint64_t* g_pos = nullptr;   // [G+1]

@@ -119,11 +119,17 @@ def test_next_use_equal(pair):
         assert t.sweep_range(w) == o.sweep_range(w), (name, w)
 
 
+def _max_group(o, d):
+    # the largest block set one call (or migration / prefetch group) brings to a node: below it a
+    # capacity is SAGA_ERR_CAPACITY, from it up to W_lo - 1 it is infeasible-epoch data
+    return max([int(o.stream(w)["groups"][:, 1].max()) for w in range(d.n_nodes) if o.stream(w)["groups"].size] or [1])
+
+
 def _caps_for(o, d, name):
     wlo = max(o.sweep_range(w)[0] for w in range(d.n_nodes))
     whi = max(o.sweep_range(w)[1] for w in range(d.n_nodes))
     caps = sweep_caps(wlo, whi, 5)
-    caps += [max(1, wlo - 1), whi + 7]
+    caps += [max(_max_group(o, d), wlo - 1, 1), whi + 7]
     return sorted(set(c for c in caps if c > 0))
 
 
@@ -306,6 +312,13 @@ def test_state_errors():
     with pytest.raises(saga.SagaError) as ex:
         t.replay(dict(policy_mask=1), [0], [0], c)
     assert ex.value.status == 3
+    # C1's largest call touches 12 blocks (S:209 CapacityError below it); 12 .. W_lo - 1 = 21 is
+    # data: the replay stops at the first epoch whose requests exceed the capacity
+    with pytest.raises(saga.SagaError) as ex:
+        t.replay(dict(policy_mask=1), [11], [0], c)
+    assert ex.value.status == 3
+    t.replay(dict(policy_mask=1), [21], [0], c)
+    assert int(c[0, 0, 0, saga.CI["INFEASIBLE_EPOCH"]]) > 0
 
 
 def test_launches_counted():
