@@ -402,7 +402,10 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
-    shard = args.shard or ("trials" if world > 1 else "nodes")
+    # N > 1 default: SURVEY §8(e)'s partition -- rank r owns cache nodes w mod R of the one trace
+    # (placement replicated, (W_lo, W_hi) max- and counters sum-all-reduced over NCCL: counters
+    # bit-identical to N = 1).  --shard trials runs an independent seeded trial per rank instead.
+    shard = args.shard or "nodes"
     trials = shard == "trials"
     seed = None
     if trials and rank > 0 and args.config != "C1":
@@ -419,7 +422,10 @@ def main():
     # keeps up to inflight expanded traces resident -- only when they fit (C1-C3); larger
     # configs chain a step's expansion to the previous step's freed trace.
     overlap = desc.n_accesses < 3 * 10 ** 8 and not args.no_overlap
-    inflight = max(1, args.inflight or (3 if overlap else 2))
+    # node-sharded ranks hold 1/R of the replay items but the same per-step placement and critical
+    # path (one item's epoch chain), so more steps are kept in flight as R grows
+    inflight = max(1, args.inflight or ((3 + (world - 1 if shard == "nodes" else 0)) if overlap else 2))
+    inflight = min(inflight, 8)
     # one stream, trace handle and communicator per in-flight step (see run_steps)
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
     comm = comms[0]
