@@ -424,8 +424,9 @@ def main():
     overlap = desc.n_accesses < 3 * 10 ** 8 and not args.no_overlap
     # node-sharded ranks hold 1/R of the replay items but the same per-step placement and critical
     # path (one item's epoch chain), so more steps are kept in flight as R grows
-    inflight = max(1, args.inflight or ((3 + (world - 1 if shard == "nodes" else 0)) if overlap else 2))
-    inflight = min(inflight, 8)
+    # (latency of one step ~ 2.4x a rank's SM-time per step at C2 when R ranks split the items)
+    inflight = max(1, args.inflight or (((3 if world == 1 or shard != "nodes" else 2 + 2 * world)) if overlap else 2))
+    inflight = min(inflight, 12)
     # one stream, trace handle and communicator per in-flight step (see run_steps)
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
     comm = comms[0]
@@ -599,13 +600,16 @@ def main():
     barrier()
     launches = saga.kernel_launches() - l0
     clocks = sampler.stop()
-    # per-kernel-family device times: the same steps again with the library's event profile on
-    # (CUDA events around every kernel family; kept out of the timed region above)
+    # per-kernel-family device times: the same steps again, one at a time, with the library's event
+    # profile on (CUDA events around every kernel family; kept out of the timed region above)
     import ctypes as C
     prof_steps = args.steps if desc.n_calls < 1_000_000 else 1
     saga.lib.saga_profile_enable(1)
     saga.lib.saga_profile_read(None, None)
-    ms_prof, _ = run_steps(prof_steps, dd)
+    ms_prof = 0.0
+    for _ in range(prof_steps):  # one step at a time: a kernel family's events must not span waits for SMs
+        ms1, _ = run_steps(1, dd)
+        ms_prof += ms1 / prof_steps
     pm = (C.c_double * len(PROF_NAMES))()
     pn = (C.c_uint64 * len(PROF_NAMES))()
     saga.lib.saga_profile_read(pm, pn)

@@ -240,7 +240,7 @@ saga_status saga_belady_next_use(saga_trace* t, uint32_t node, uint32_t* next_us
 
 /* A4 for several owned nodes at once (no outputs; results kept as by saga_belady_next_use): the
  * nodes' streams are sorted and scanned as segments of one launch per kernel (K4 onesweep passes,
- * K5 segmented scan, per-epoch statistics), in batches of up to 32 nodes / 2^30 accesses.  A node
+ * K5 segmented scan, per-epoch statistics), in batches of up to 32 nodes / 2^29 accesses.  A node
  * already done is skipped.  Syncs once per batch (sizes of the derived tables). */
 saga_status saga_belady_next_use_nodes(saga_trace* t, const uint32_t* nodes, uint32_t n_nodes, saga_stream_t stream);
 

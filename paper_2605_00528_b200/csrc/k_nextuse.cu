@@ -480,11 +480,12 @@ saga_status next_use_batch(saga_trace* t, const std::vector<uint32_t>& ws, cudaS
 
 }  // namespace
 
-// A4 for several nodes: batches of at most MAXN nodes and ~2^30 accesses (scratch ~24 B/access)
+// A4 for several nodes: batches of at most MAXN nodes and ~2^29 accesses (scratch ~24 B/access,
+// held by the workspace cache afterwards)
 saga_status run_next_use_nodes(saga_trace* t, const uint32_t* nodes, uint32_t n, cudaStream_t s) {
   std::vector<uint32_t> batch;
   uint64_t acc = 0;
-  const uint64_t cap = 1ull << 30;
+  const uint64_t cap = 1ull << 29;
   for (uint32_t i = 0; i <= n; ++i) {
     const bool flush = i == n || batch.size() == MAXN || (!batch.empty() && acc + t->nodes[nodes[i]].N > cap);
     if (flush && !batch.empty()) {

@@ -87,6 +87,19 @@ struct __align__(16) ListRec {
   int64_t t;
   uint32_t u, pa, pe, lo, kp, flags;
 };
+// A live-unit list: the first LC entries live in shared memory, the rest in the CTA's global
+// scratch (the list is read by four passes per AEG eviction epoch: shared memory turns those
+// round trips into ~30-cycle loads while nL <= LC, the common case)
+#ifndef SAGA_REPLAY_LC
+#define SAGA_REPLAY_LC 256
+#endif
+constexpr uint32_t LC = SAGA_REPLAY_LC;
+struct LView {
+  ListRec* s;
+  ListRec* g;
+  __device__ __forceinline__ ListRec& operator[](uint32_t i) const { return i < LC ? s[i] : g[i]; }
+};
+
 // per-call inputs of the WA-LRU key of a private session whose newest call is c
 struct __align__(8) CallKey {
   int64_t tend;     // tool start (Alg. 1 elapsed-time origin)
@@ -225,6 +238,62 @@ __device__ __forceinline__ void hb_clear(const HB& h, uint32_t i) {
   atomicSub(&h.c1[i >> 10], 1u);
   atomicSub(&h.c2[i >> 20], 1u);
 }
+// Grouping lanes by target word for one atomic per word: positions and local ids come in runs,
+// so usually every active lane hits the same word -- one shuffle and one vote detect that and a
+// single atomic carries the whole warp; otherwise each lane issues its own atomic (atomics
+// commute: the result is the same; MATCH.ANY, which the general grouping needs, costs more than
+// the handful of separate atomics of the rare mixed warp).
+#ifndef SAGA_REPLAY_MATCH_ANY
+// Warp-collective (all lanes call): lanes with `act` set (or clear) bit `idx` of `bits`.
+__device__ __forceinline__ void warp_bits(uint32_t* bits, bool act, uint32_t idx, bool set) {
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  if (!am) return;
+  const uint32_t w = idx >> 5;
+  const uint32_t w0 = __shfl_sync(0xffffffffu, w, __ffs(am) - 1);
+  if (__all_sync(0xffffffffu, !act || w == w0)) {
+    const uint32_t m = __reduce_or_sync(0xffffffffu, act ? 1u << (idx & 31) : 0u);
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(am) - 1)) {
+      if (set) atomicOr(&bits[w0], m);
+      else atomicAnd(&bits[w0], ~m);
+    }
+  } else if (act) {
+    if (set) atomicOr(&bits[w], 1u << (idx & 31));
+    else atomicAnd(&bits[w], ~(1u << (idx & 31)));
+  }
+}
+// Warp-collective: lanes with `act` add (or subtract) 1 to counts[key].
+__device__ __forceinline__ void warp_count(uint32_t* counts, bool act, uint32_t key, bool add) {
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  if (!am) return;
+  const uint32_t k0 = __shfl_sync(0xffffffffu, key, __ffs(am) - 1);
+  if (__all_sync(0xffffffffu, !act || key == k0)) {
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(am) - 1)) {
+      const uint32_t n = __popc(am);
+      atomicAdd(&counts[k0], add ? n : (uint32_t)(-(int32_t)n));
+    }
+  } else if (act) {
+    atomicAdd(&counts[key], add ? 1u : 0xFFFFFFFFu);
+  }
+}
+// warp-collective update of a hierarchical bitmap: bits, then the c1 / c2 counts
+__device__ __forceinline__ void hb_update_warp(const HB& h, bool act, uint32_t i, bool set) {
+  const uint32_t am = __ballot_sync(0xffffffffu, act);
+  if (!am) return;
+  warp_bits(h.bits, act, i, set);
+  const uint32_t c0 = __shfl_sync(0xffffffffu, i >> 10, __ffs(am) - 1);
+  const uint32_t d = set ? 1u : 0xFFFFFFFFu;
+  if (__all_sync(0xffffffffu, !act || (i >> 10) == c0)) {
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(am) - 1)) {
+      const uint32_t n = __popc(am);
+      atomicAdd(&h.c1[c0], set ? n : (uint32_t)(-(int32_t)n));
+      atomicAdd(&h.c2[c0 >> 10], set ? n : (uint32_t)(-(int32_t)n));
+    }
+  } else if (act) {
+    atomicAdd(&h.c1[i >> 10], d);
+    atomicAdd(&h.c2[i >> 20], d);
+  }
+}
+#else
 // Warp-collective (all lanes call): lanes with `act` set (or clear) bit `idx` of `bits`; one
 // atomic per distinct word (lanes usually hit few words: positions and local ids come in runs).
 __device__ __forceinline__ void warp_bits(uint32_t* bits, bool act, uint32_t idx, bool set) {
@@ -262,6 +331,8 @@ __device__ __forceinline__ void hb_update_warp(const HB& h, bool act, uint32_t i
   }
 }
 
+#endif
+
 // Warp-collective (all lanes call): each lane appends idx(b) | tag for every set bit b of
 // `bits` (bit b of word wi is index wi * 32 + b) to the victim list.
 __device__ __forceinline__ void emit_bits(uint32_t* vlist, uint32_t* n_vict, uint32_t wi, uint32_t bits, uint32_t tag) {
@@ -293,18 +364,27 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
       const uint32_t ci = i0 + lane;
       const uint32_t cv = ci < hi ? h.c1[ci] : 0u;
       uint32_t nz = __ballot_sync(0xffffffffu, cv != 0);
-      while (nz) {
-        const int l = __ffs(nz) - 1;
-        nz &= nz - 1;
-        const uint32_t c1i = i0 + l;
-        const uint32_t wi = c1i * 32u + lane;
-        const uint32_t m = wi > tw ? 0xffffffffu : (wi == tw ? ~((1u << (T & 31)) - 1u) : 0u);
-        const uint32_t wv = h.bits[wi];
-        const uint32_t tk = wv & m;
-        if (tk) h.bits[wi] = wv & ~m;
-        emit_bits(vlist, n_vict, wi, tk, tag);
-        const uint32_t n = warp_sum(__popc(tk));
-        if (lane == 0 && n) { h.c1[c1i] -= n; atomicSub(&h.c2[jb], n); }
+      while (nz) {  // up to 4 non-empty c1 blocks at a time: their word loads are issued together
+        uint32_t c1i[4], wv[4];
+        int nb = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          c1i[b] = NONE;
+          if (nz) { c1i[b] = i0 + (uint32_t)(__ffs(nz) - 1); nz &= nz - 1; ++nb; }
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) wv[b] = c1i[b] != NONE ? h.bits[c1i[b] * 32u + lane] : 0u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b >= nb) break;
+          const uint32_t wi = c1i[b] * 32u + lane;
+          const uint32_t m = wi > tw ? 0xffffffffu : (wi == tw ? ~((1u << (T & 31)) - 1u) : 0u);
+          const uint32_t tk = wv[b] & m;
+          if (tk) h.bits[wi] = wv[b] & ~m;
+          emit_bits(vlist, n_vict, wi, tk, tag);
+          const uint32_t n = warp_sum(__popc(tk));
+          if (lane == 0 && n) { h.c1[c1i[b]] -= n; atomicSub(&h.c2[jb], n); }
+        }
       }
     }
   }
@@ -467,7 +547,9 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
   uint32_t* alive = reinterpret_cast<uint32_t*>(base + a.o_bits);   // AEG / EVICT_ALL (aliases pend.bits)
   uint32_t* nres_a = reinterpret_cast<uint32_t*>(base + a.o_nres);  // AEG / EVICT_ALL next-use-resident bits
   uint32_t* vunits = reinterpret_cast<uint32_t*>(base + a.o_vu);    // AEG: list entries evicted this epoch
-  ListRec* lists[2] = {reinterpret_cast<ListRec*>(base + a.o_list0), reinterpret_cast<ListRec*>(base + a.o_list1)};
+  __shared__ ListRec s_list[2][LC];
+  const LView lists[2] = {{s_list[0], reinterpret_cast<ListRec*>(base + a.o_list0)},
+                          {s_list[1], reinterpret_cast<ListRec*>(base + a.o_list1)}};
   uint64_t* kbuf = reinterpret_cast<uint64_t*>(base + a.o_kbuf);
   uint32_t* vlist = reinterpret_cast<uint32_t*>(base + a.o_vl);
   const CallKey* ck = a.callkey;
@@ -746,7 +828,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           // every resident non-in-flight block has one bit; k <= |cand| because |A| <= C
           hb_take_top(rec, k, vlist, 0u, sm, a.dbg);
         } else {
-          ListRec* L = lists[cur];
+          const LView L = lists[cur];
           // whole-unit eviction: list every resident latest position of unit u (warp-collective)
           auto evict_unit = [&](uint32_t u, uint32_t pa, uint32_t pe, bool prot) {
             const uint32_t wlast = (pe - 1) >> 5;
@@ -1001,7 +1083,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       // ---- live unit list: append this epoch's units; every 16th epoch also drop the units
       // whose count reached 0 (until then the passes skip them: each one tests cnt first) ----
       if (units && (j & 15u) != 15u) {
-        ListRec* L = lists[cur];
+        const LView L = lists[cur];
         const uint32_t U0 = nd.ev_unit[j], U1 = nd.ev_unit[j + 1];
         for (uint32_t i = threadIdx.x; i < U1 - U0; i += RT) {
           const UnitRec ur = nd.urec[U0 + i];
@@ -1012,8 +1094,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
         nL += U1 - U0;  // read again only after the next epoch's first barrier
       } else if (units) {
         __syncthreads();
-        const ListRec* L = lists[cur];
-        ListRec* L2 = lists[cur ^ 1];
+        const LView L = lists[cur];
+        const LView L2 = lists[cur ^ 1];
         const uint32_t U0 = nd.ev_unit[j], U1 = nd.ev_unit[j + 1];
         const uint32_t tot = nL + (U1 - U0);
         for (uint32_t i = threadIdx.x; i < ((tot + 31) & ~31u); i += RT) {
@@ -1410,7 +1492,9 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   uint32_t grid = std::min<uint32_t>(n_items, (uint32_t)nsm * (uint32_t)std::max(occ, 1));
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const uint64_t budget = free_b > (4ull << 30) ? (free_b - (4ull << 30)) / 2 : free_b / 4;
+  // idle blocks of the workspace cache are released by ws_malloc when the scratch needs them
+  const uint64_t avail = (uint64_t)free_b + ws_idle_bytes();
+  const uint64_t budget = avail > (4ull << 30) ? (avail - (4ull << 30)) / 10 * 8 : avail / 4;
   grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(grid, budget / std::max<uint64_t>(a.cta_bytes, 1)));
   const bool trace = getenv("SAGA_REPLAY_TRACE") != nullptr;
   NodeArr* d_nodes = nullptr;

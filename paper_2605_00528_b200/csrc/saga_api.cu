@@ -120,6 +120,19 @@ void ws_free(void* p, cudaStream_t s) {
     if (b.p == p) { b.used = false; b.s = s; b.any = false; return; }
 }
 
+// bytes held by idle cached blocks of the current device (ws_malloc releases them when a fresh
+// allocation does not fit): memory a large allocation can count on besides cudaMemGetInfo's free
+size_t ws_idle_bytes() {
+  using namespace ws_detail;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  size_t n = 0;
+  for (const Blk& b : g_ws)
+    if (!b.used && b.dev == dev) n += b.size;
+  return n;
+}
+
 // after the caller synchronised stream s: its idle blocks may serve any stream
 void ws_release_stream(cudaStream_t s) {
   using namespace ws_detail;

@@ -34,6 +34,7 @@ void set_error(const char* fmt, ...);
 cudaError_t ws_malloc(void** p, size_t bytes, cudaStream_t s);
 void ws_free(void* p, cudaStream_t s);
 void ws_release_stream(cudaStream_t s);  // after a sync of s: its idle blocks serve any stream
+size_t ws_idle_bytes();                   // idle cached bytes of the current device
 
 // Small host<->device copies of the host-side control flow (sizes, flags, launch tables).  Both
 // wait for the stream first and move the bytes through a pinned bounce buffer, then wait again:
