@@ -87,19 +87,6 @@ struct __align__(16) ListRec {
   int64_t t;
   uint32_t u, pa, pe, lo, kp, flags;
 };
-// A live-unit list: the first LC entries live in shared memory, the rest in the CTA's global
-// scratch (the list is read by four passes per AEG eviction epoch: shared memory turns those
-// round trips into ~30-cycle loads while nL <= LC, the common case)
-#ifndef SAGA_REPLAY_LC
-#define SAGA_REPLAY_LC 256
-#endif
-constexpr uint32_t LC = SAGA_REPLAY_LC;
-struct LView {
-  ListRec* s;
-  ListRec* g;
-  __device__ __forceinline__ ListRec& operator[](uint32_t i) const { return i < LC ? s[i] : g[i]; }
-};
-
 // per-call inputs of the WA-LRU key of a private session whose newest call is c
 struct __align__(8) CallKey {
   int64_t tend;     // tool start (Alg. 1 elapsed-time origin)
@@ -547,9 +534,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
   uint32_t* alive = reinterpret_cast<uint32_t*>(base + a.o_bits);   // AEG / EVICT_ALL (aliases pend.bits)
   uint32_t* nres_a = reinterpret_cast<uint32_t*>(base + a.o_nres);  // AEG / EVICT_ALL next-use-resident bits
   uint32_t* vunits = reinterpret_cast<uint32_t*>(base + a.o_vu);    // AEG: list entries evicted this epoch
-  __shared__ ListRec s_list[2][LC];
-  const LView lists[2] = {{s_list[0], reinterpret_cast<ListRec*>(base + a.o_list0)},
-                          {s_list[1], reinterpret_cast<ListRec*>(base + a.o_list1)}};
+  ListRec* lists[2] = {reinterpret_cast<ListRec*>(base + a.o_list0), reinterpret_cast<ListRec*>(base + a.o_list1)};
   uint64_t* kbuf = reinterpret_cast<uint64_t*>(base + a.o_kbuf);
   uint32_t* vlist = reinterpret_cast<uint32_t*>(base + a.o_vl);
   const CallKey* ck = a.callkey;
@@ -828,7 +813,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           // every resident non-in-flight block has one bit; k <= |cand| because |A| <= C
           hb_take_top(rec, k, vlist, 0u, sm, a.dbg);
         } else {
-          const LView L = lists[cur];
+          ListRec* L = lists[cur];
           // whole-unit eviction: list every resident latest position of unit u (warp-collective)
           auto evict_unit = [&](uint32_t u, uint32_t pa, uint32_t pe, bool prot) {
             const uint32_t wlast = (pe - 1) >> 5;
@@ -1083,7 +1068,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
       // ---- live unit list: append this epoch's units; every 16th epoch also drop the units
       // whose count reached 0 (until then the passes skip them: each one tests cnt first) ----
       if (units && (j & 15u) != 15u) {
-        const LView L = lists[cur];
+        ListRec* L = lists[cur];
         const uint32_t U0 = nd.ev_unit[j], U1 = nd.ev_unit[j + 1];
         for (uint32_t i = threadIdx.x; i < U1 - U0; i += RT) {
           const UnitRec ur = nd.urec[U0 + i];
@@ -1094,8 +1079,8 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
         nL += U1 - U0;  // read again only after the next epoch's first barrier
       } else if (units) {
         __syncthreads();
-        const LView L = lists[cur];
-        const LView L2 = lists[cur ^ 1];
+        const ListRec* L = lists[cur];
+        ListRec* L2 = lists[cur ^ 1];
         const uint32_t U0 = nd.ev_unit[j], U1 = nd.ev_unit[j + 1];
         const uint32_t tot = nL + (U1 - U0);
         for (uint32_t i = threadIdx.x; i < ((tot + 31) & ~31u); i += RT) {

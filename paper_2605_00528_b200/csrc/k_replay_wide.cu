@@ -12,9 +12,6 @@
 #define SAGA_REPLAY_MINB SAGA_WIDE_MINB
 #define SAGA_REPLAY_PF SAGA_WIDE_PF
 #define SAGA_REPLAY_DYN_KB SAGA_WIDE_DYN_KB
-#ifndef SAGA_REPLAY_LC
-#define SAGA_REPLAY_LC 128
-#endif
 #define SAGA_REPLAY_ENTRY run_replay_wide
 #define SAGA_REPLAY_IS_WIDE 1
 #include "k_replay.cu"
