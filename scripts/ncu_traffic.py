@@ -36,9 +36,11 @@ def main(csv_path, config, out="profiles/ncu_traffic.json"):
     db = json.load(open(out)) if os.path.exists(out) else {}
     db = {k: v for k, v in db.items() if k.startswith("C")}
     cfg = {}
+    bulk = {"score_aeg", "score_belady", "select"}   # per launch: the profiled command repeats these
     for f, v in fam.items():
-        cfg[f] = v["bytes"]          # per step (the profiled command runs one step / one bulk launch)
-        cfg[f + "_ms"] = v["ns"] / 1e6
+        div = v["launches"] if f in bulk else 1          # pipeline families: per step (one step profiled)
+        cfg[f] = v["bytes"] / div
+        cfg[f + "_ms"] = v["ns"] / 1e6 / div
         if f == "replay" and v["inst"]:
             cfg["replay_warp_inst"] = v["inst"]
     cfg["_source"] = f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum " \
