@@ -628,10 +628,13 @@ def main():
         torch.cuda.synchronize()
         out_host = [torch.empty(tuple(ctr.shape), dtype=torch.int64, pin_memory=True) for _ in range(inflight)]
 
+        wrote = set()
+
         def d2h(i, c2):  # the step's result back to the host, inside the timed region
             with torch.cuda.stream(streams[i]):
                 out_host[i].copy_(c2, non_blocking=True)
             streams[i].synchronize()
+            wrote.add(i)
 
         ems, _ = run_steps(args.steps, host_pinned, d2h=d2h)
         barrier()
@@ -641,8 +644,8 @@ def main():
         ems = float(et[0])
         e2e = {"value": replay_accesses / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": host_pinned.nbytes,
                "d2h_bytes_per_step": int(out_host[0].numel() * 8), "ms_per_step": ems}
-        for oh in out_host:
-            assert np.array_equal(oh.numpy(), counters_host), "e2e counters differ from the device-resident run"
+        for i in sorted(wrote):  # (streams without a step when steps < steps in flight hold nothing)
+            assert np.array_equal(out_host[i].numpy(), counters_host), "e2e counters differ from the device-resident run"
 
     # ---- roofline of the dominant kernel family (per-launch, CUDA events on the launching stream) ----
     peak, peak_kind = hbm_peak()
@@ -701,9 +704,15 @@ def main():
         bulk = bulk_score_select(t_b, desc, stream, dev)
         t_b.free()
         if bulk:
+            n_cand = 1024 * 32768
             for kname, kv in bulk.items():
                 if isinstance(kv, dict):
                     kv["frac"] = kv["algorithmic_gb_s"] / peak
+                    kv["input_over_l2"] = (n_cand * (12 if kname == "score_aeg" else 8) / l2_bytes) if l2_bytes else None
+                    tr = ncu_cfg.get(kname)  # ncu DRAM bytes of one launch of the same snapshot
+                    if tr:
+                        kv["ncu_dram_bytes"] = tr
+                        kv["traffic_over_algorithmic"] = tr / (n_cand * kv["bytes_per_candidate"])
         pat = f3_pattern(stream, dev)
         pat["frac"] = pat["algorithmic_gb_s"] / peak
         f4 = f4_tool_stats(stream, dev)

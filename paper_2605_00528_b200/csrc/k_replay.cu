@@ -504,7 +504,10 @@ __device__ __forceinline__ uint32_t owner_size(const TraceView& v, const CallKey
   } while (0)
 
 constexpr uint32_t VT_LID = 0x80000000u;  // victim-list tag: the entry is a local id, else a position
-constexpr int UNR = 2;                    // record chunks whose loads are issued together (R2 / R4)
+#ifndef SAGA_REPLAY_UNR
+#define SAGA_REPLAY_UNR 2
+#endif
+constexpr int UNR = SAGA_REPLAY_UNR;      // record chunks whose loads are issued together (R2 / R4)
 
 __device__ __forceinline__ uint32_t unit_mask(uint32_t wi, uint32_t pa, uint32_t pe) {
   uint32_t m = 0xffffffffu;

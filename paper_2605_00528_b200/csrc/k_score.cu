@@ -67,8 +67,33 @@ __device__ __forceinline__ OwnerKeyIn owner_at(const TraceView& v, uint32_t o, u
   return r;
 }
 
+// owner reference of a candidate, resolved once in pass 1: the session's current call c*, or
+// CREF_SHARED | type for a shared-prefix block
+constexpr uint32_t CREF_SHARED = 0x80000000u;
+constexpr uint32_t SC_STAGE = 32768;  // candidates per segment whose owner reference is kept in shared memory
+
+__device__ __forceinline__ OwnerKeyIn owner_of_ref(const TraceView& v, uint32_t ref, uint32_t act) {
+  OwnerKeyIn r;
+  if (ref & CREF_SHARED) {
+    const uint32_t t = ref & ~CREF_SHARED;
+    const bool on = (act >> t) & 1u;
+    r.shared = true; r.prot_shared = on; r.size = __ldg(&v.tlen[t]); r.P = on ? 1.0f : 0.0f;
+    r.fin = false; r.t_call = 0; r.ttl_base = 0;
+    return r;
+  }
+  const uint32_t c = ref;  // independent loads: one round trip per run of one session's blocks
+  r.shared = false; r.prot_shared = false;
+  r.size = __ldg(&v.ci_size[c]);
+  r.fin = __ldg(&v.ci_fin[c]) != 0;
+  r.P = __ldg(&v.ci_P[c]);
+  r.t_call = __ldg(&v.tend[c]);
+  r.ttl_base = call_ttl_base(v, c);
+  return r;
+}
+
 __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
   __shared__ BlockScratch<ST> sm;
+  extern __shared__ uint32_t s_cref[];  // [SC_STAGE] owner reference per candidate of the segment
   Par par;
   const TraceView& v = a.v;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -91,10 +116,12 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
     const uint64_t n = c1 - c0;
     const uint64_t slab = ((n + SW - 1) / SW + 31) & ~31ull;
     const uint64_t w0 = c0 + (uint64_t)wid * slab, w1 = min(c1, w0 + slab);
-    // pass 1: normalisers (eq:recency tau_max, eq:size size_max)
+    // pass 1: normalisers (eq:recency tau_max, eq:size size_max); each candidate's owner
+    // reference (c* or the shared type) is kept for pass 2 when the segment fits
+    const bool stage = n <= SC_STAGE;
     long long tau = 0;
     uint32_t smax = 1;
-    uint32_t last_o = NONE, last_sz = 0;
+    uint32_t last_o = NONE, last_sz = 0, last_ref = 0;
     for (uint64_t b = w0; b < w1; b += 32 * SU) {
       uint32_t lid[SU];
       int64_t tl[SU];
@@ -111,8 +138,15 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
         const uint32_t o = __ldg(&lown[lid[u]]);
         if (o != last_o) {
           last_o = o;
-          last_sz = o >= v.n_sessions ? __ldg(&v.tlen[o - v.n_sessions]) : __ldg(&v.ci_size[cstar(v, o, e)]);
+          if (o >= v.n_sessions) {
+            last_ref = CREF_SHARED | (o - v.n_sessions);
+            last_sz = __ldg(&v.tlen[o - v.n_sessions]);
+          } else {
+            last_ref = cstar(v, o, e);
+            last_sz = __ldg(&v.ci_size[last_ref]);
+          }
         }
+        if (stage) s_cref[b + (uint64_t)u * 32 + lane - c0] = last_ref;
         smax = max(smax, last_sz);
       }
     }
@@ -123,8 +157,9 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
     x.den = (int64_t)(a.p_high - a.p_low) * C;
     x.num = min(x.den, max((int64_t)0, 1000 * (int64_t)occ - (int64_t)a.p_low * C));
     x.ttl_max = a.ttl_max; x.alpha = a.alpha; x.beta = a.beta; x.gamma = a.gamma;
-    // pass 2: keys (the slab re-read hits L2)
+    // pass 2: keys (the slab re-read hits L2; owner references from shared memory)
     last_o = NONE;
+    last_ref = NONE;
     OwnerKeyIn oi{};
     for (uint64_t b = w0; b < w1; b += 32 * SU) {
       uint32_t lid[SU];
@@ -139,8 +174,13 @@ __global__ void __launch_bounds__(ST) k_score(ScoreArgs a) {
       for (int u = 0; u < SU; ++u) {
         if (lid[u] == NONE) continue;
         const uint64_t i = b + (uint64_t)u * 32 + lane;
-        const uint32_t o = __ldg(&lown[lid[u]]);
-        if (o != last_o) { last_o = o; oi = owner_at(v, o, e, act); }
+        if (stage) {
+          const uint32_t ref = s_cref[i - c0];
+          if (ref != last_ref) { last_ref = ref; oi = owner_of_ref(v, ref, act); }
+        } else {
+          const uint32_t o = __ldg(&lown[lid[u]]);
+          if (o != last_o) { last_o = o; oi = owner_at(v, o, e, act); }
+        }
         const float sc = wa_lru_score(x, tl[u], oi.size, oi.P);
         __stcs(&a.key[i], aeg_key(ttl_protected(x, oi), quantize_q20(sc), lid[u]));
         if (a.score) __stcs(&a.score[i], sc);
@@ -373,7 +413,9 @@ saga_status run_score(const saga_trace* t, const saga_score_batch* b, const saga
     const bool vec = ((uintptr_t)b->cand_lid % 16 == 0) && ((uintptr_t)b->cand_nu % 16 == 0) && ((uintptr_t)key % 16 == 0);
     k_key_belady<<<nsm_count() * 8, 256, 0, s>>>(b->cand_lid, b->cand_nu, b->seg_off, b->n_seg, vec, key);
   } else {
-    k_score<<<std::min<unsigned>(b->n_seg, nsm_count()), ST, 0, s>>>(a);
+    const size_t dyn = (size_t)SC_STAGE * 4;
+    SAGA_CK(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k_score<<<std::min<unsigned>(b->n_seg, nsm_count()), ST, dyn, s>>>(a);
   }
   prof_end(SAGA_PROF_SCORE, s);
   count_launch();

@@ -202,6 +202,9 @@ __global__ void __launch_bounds__(SORT_T, 4) k_onesweep(const __grid_constant__ 
     } else if (__all_sync(0xffffffffu, d == ((d0 + (uint32_t)lane) & (RADIX - 1)))) {
       peers = 1u << lane;
     } else {
+#ifdef SAGA_SORT_MATCH_ANY
+      peers = __match_any_sync(0xffffffffu, d);
+#else
       peers = 0xffffffffu;
 #pragma unroll
       for (int b = 0; b < RBITS + 1; ++b) {
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(SORT_T, 4) k_onesweep(const __grid_constant__ 
         const uint32_t bal = __ballot_sync(0xffffffffu, bit);
         peers &= bit ? bal : ~bal;
       }
+#endif
     }
     const uint32_t leader = 31 - __clz(peers);
     uint32_t c = 0;
