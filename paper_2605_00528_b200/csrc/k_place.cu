@@ -94,14 +94,16 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   SessRec* sess = SS ? reinterpret_cast<SessRec*>(smem_raw) : a.sess_g;
   uint8_t* moved = SS ? smem_raw + (size_t)NS * sizeof(SessRec) : a.moved_g;
   size_t off = SS ? (((size_t)NS * (sizeof(SessRec) + 1) + 15) & ~(size_t)15) : 0;
-  int64_t* sF = reinterpret_cast<int64_t*>(smem_raw + off) + (size_t)lane * K;     // S: finish thresholds
-  off += (size_t)W * K * 8;
-  uint32_t* sS = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * K;   // S: sessions
-  off += (size_t)W * K * 4;
+  // S lives in slots [sh, sh + nS) of a 2K-slot array (compacted to slot 0 when the tail is full)
+  int64_t* sF = reinterpret_cast<int64_t*>(smem_raw + off) + (size_t)lane * 2 * K;  // S: finish thresholds
+  off += (size_t)W * 2 * K * 8;
+  uint32_t* sS = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * 2 * K;  // S: sessions
+  off += (size_t)W * 2 * K * 4;
   uint32_t* wS = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * Q;   // W: sessions (ring)
   off += (size_t)W * Q * 4;
   uint32_t* wR = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * Q;   // W: work (us)
   __shared__ int32_t cnt[32][32];                       // sessions with aff = w, !fin, by type
+  __shared__ __align__(16) SessRec b_st[32];            // P3 batch: post-state of call next + i
   // call records streamed ahead by TMA bulk copies: chunk j (calls [256 j, 256 j + 256)) lives
   // in buffer j & 1; chunk j + 1 is requested when chunk j is first touched
   constexpr uint32_t CH = 256;
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     }
   };
   const bool act_lane = lane < W;
-  uint32_t nS = 0, nW = 0, wh = 0, sh = 0;  // |S|, |W|, ring heads of W and S (S is a ring of K)
+  uint32_t nS = 0, nW = 0, wh = 0, sh = 0;  // |S|, |W|, ring head of W, first slot of S
   int64_t V = 0, LW = 0, L = 0, idle = 0;
   uint32_t next = 0;
   uint64_t e = 1;
@@ -166,51 +168,37 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   load_ps();
 
   auto w_at = [&](uint32_t i) { uint32_t j = wh + i; return j >= Q ? j - Q : j; };
-  auto s_at = [&](uint32_t i) { uint32_t j = sh + i; return j >= K ? j - K : j; };
   // insert a call into S keeping F ascending (new calls usually land at the tail)
   auto s_insert = [&](uint32_t sid, int64_t F) {
-    uint32_t i = nS;
-    while (i > 0) {
-      const uint32_t jp = s_at(i - 1);
-      if (sF[jp] <= F) break;
-      const uint32_t j = s_at(i);
-      sF[j] = sF[jp]; sS[j] = sS[jp];
-      --i;
+    if (sh + nS == 2 * K) {  // tail full: move S down to slot 0 (sh >= K, so at most once per K completions)
+      for (uint32_t i = 0; i < nS; ++i) { sF[i] = sF[sh + i]; sS[i] = sS[sh + i]; }
+      sh = 0;
     }
-    const uint32_t j = s_at(i);
-    sF[j] = F; sS[j] = sid; ++nS;
+    uint32_t i = sh + nS;
+    while (i > sh && sF[i - 1] > F) { sF[i] = sF[i - 1]; sS[i] = sS[i - 1]; --i; }
+    sF[i] = F; sS[i] = sid; ++nS;
   };
   // move waiting calls into service while a server is free (FIFO order)
   auto admit = [&]() {
     while (nS < K && nW > 0) {
-      const uint32_t j = w_at(0);
-      const int64_t r = wR[j];
+      const int64_t r = wR[wh];
       LW -= min(r, E);
-      s_insert(wS[j], V + r);
+      s_insert(wS[wh], V + r);
       wh = w_at(1); --nW;
     }
   };
-  // drop the calls of S whose threshold is reached (a prefix); returns the work they had left
-  auto complete = [&](int64_t Vnew, int64_t Vold, int64_t& served) -> uint32_t {
-    uint32_t m = 0;
-    while (nS > 0) {
-      const uint32_t j = s_at(0);
-      if (sF[j] > Vnew) break;
-      served += sF[j] - Vold;
-      moved[sS[j]] = 0;
-      sh = s_at(1); --nS; ++m;
-    }
-    return m;
+  // drop the calls of S whose threshold is reached (a prefix)
+  auto complete = [&](int64_t Vnew) {
+    while (nS > 0 && sF[sh] <= Vnew) { moved[sS[sh]] = 0; ++sh; --nS; }
   };
+  // load(w) = sum over the queue of min(rem, E): calls of S with F - V < E form a prefix
   auto load_of = [&]() {
-    int64_t l = LW;
-    uint32_t i = 0;
-    for (; i < nS; ++i) {
-      const int64_t r = sF[s_at(i)] - V;
+    int64_t l = LW + (int64_t)nS * E;
+    for (uint32_t j = sh; j < sh + nS; ++j) {
+      const int64_t r = sF[j] - V;
       if (r >= E) break;
-      l += r;
+      l -= E - r;
     }
-    l += (int64_t)(nS - i) * E;
     return l;
   };
   // oldest waiting call of a session that is not `moved` and has no call in service here
@@ -219,29 +207,29 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
       const uint32_t s = wS[w_at(i)];
       if (moved[s]) continue;
       bool busy = false;
-      for (uint32_t j = 0; j < nS; ++j) if (sS[s_at(j)] == s) { busy = true; break; }
+      for (uint32_t j = sh; j < sh + nS; ++j) if (sS[j] == s) { busy = true; break; }
       if (!busy) return (int32_t)s;
     }
     return -1;
   };
 
+  bool p1_done = false;  // P1 of epoch e was applied by the previous closed-form advance
   while (true) {
-    const bool any = __ballot_sync(0xffffffffu, act_lane && (nS + nW) > 0) != 0;
-    if (next >= NC && !any) break;
     const int64_t Te = (int64_t)e * E;
     bool got = false;
     // ---------------- P1 service: the first kappa calls progress by one epoch ----------------
-    if (act_lane) {
-      admit();
-      int64_t served = 0;
-      const uint32_t m = complete(V + E, V, served);
-      served += (int64_t)nS * E;  // every remaining call in service progressed by E
-      (void)m;
-      V += E;
-      idle = served == 0 ? idle + 1 : 0;
-      L = load_of();
+    if (!p1_done) {
+      if (next >= NC && __ballot_sync(0xffffffffu, act_lane && (nS + nW) > 0) == 0) break;
+      if (act_lane) {
+        admit();
+        idle = nS == 0 ? idle + 1 : 0;  // every call in service progresses by min(r, E) > 0
+        complete(V + E);
+        V += E;
+        L = load_of();
+      }
+      __syncwarp();
     }
-    __syncwarp();
+    p1_done = false;
     // ---------------- P2 steal: idle thief AND load-ratio guard (P:361, P:766(a)) ----------------
     uint32_t thieves = __ballot_sync(0xffffffffu, act_lane && idle * E >= a.t_idle_us);
     if (thieves && __ballot_sync(0xffffffffu, act_lane && nW > 0)) {
@@ -294,8 +282,8 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           SessRec sr = sess[s];
           const uint32_t ty = v.styp[s];
           if (!(sr.ttlf & S_FIN)) {  // s is counted at its current affinity node
-            const int32_t ao = sr.aff;
-            cnt[ao][ty]--; cnt[th][ty]++;
+            cnt[sr.aff][ty]--;
+            cnt[th][ty]++;
           }
           sr.aff = (int32_t)th;
           sess[s] = sr;
@@ -311,74 +299,86 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
       if (stole) load_ps();  // affinities of prefetched sessions may have changed
     }
     // ---------------- P3 route the calls admitted at T_e (eq:routing) ----------------
+    // One batch = the calls among next .. next + 31 admitted at T_e (a prefix; lane i holds call
+    // next + i).  Each lane first evaluates cached(w*, s) for its own call from the prefetched
+    // session state; the calls are then routed in order, every lane following call i uniformly
+    // (one shuffle of lane i's packed view, the stay test, a two-step redux argmin).  A call whose
+    // session already had a call earlier in the batch reads that call's post-state from b_st.
+    // The affinity counts, reroute count and session records are updated per batch, in
+    // parallel, after the routing.
     while (next < NC && __shfl_sync(0xffffffffu, pre.e, 0) == (uint32_t)e) {
-      const uint32_t c = next + lane;
-      const bool valid = c < NC && pre.e == (uint32_t)e;
+      const bool valid = next + lane < NC && pre.e == (uint32_t)e;
       const uint32_t nb = __popc(__ballot_sync(0xffffffffu, valid));
-      const uint32_t s = pre.s, ty = pre.tyf & 0xFFFFu;
-      const bool f_new_l = (pre.tyf & F_FNEW) != 0;
-      int32_t aff = valid ? ps.aff : -1;
-      bool fin = valid && (ps.ttlf & S_FIN);
-      bool term_lv = !valid || (ps.ttlf & S_TERM);
-      int64_t tend_lv = ps.tend_lv, ttl_lv = ps.ttlf & (S_FIN - 1u);
-      const uint32_t same = __match_any_sync(0xffffffffu, valid ? s : 0xFFFFFFFFu);
+      const uint32_t same = __match_any_sync(0xffffffffu, valid ? pre.s : 0xFFFFFFFFu);
+      const uint32_t earlier = same & ((1u << lane) - 1u);
+      const bool has_later = (same & ~((2u << lane) - 1u)) != 0;
+      const int64_t cap_theta = (int64_t)a.theta_pm * (int64_t)K * E;
+      auto is_cached = [&](const SessRec& st) {  // Alg. 1 with m = 0 at the affinity node
+        return st.aff >= 0 && !(st.ttlf & S_TERM) && (Te - st.tend_lv <= (int64_t)(st.ttlf & (S_FIN - 1u)));
+      };
+      const uint32_t info = (ps.aff >= 0 ? (uint32_t)ps.aff : 0xFFu) | ((uint32_t)is_cached(ps) << 8) |
+                            ((ps.ttlf & S_FIN) ? 1u << 9 : 0u) | (earlier ? 1u << 10 : 0u) |
+                            (has_later ? 1u << 11 : 0u) | ((earlier ? 31u - __clz(earlier) : 0u) << 12);
+      uint32_t my_w = 0;
+      int32_t my_ws = -1;
+      bool my_fin = false;
       for (uint32_t i = 0; i < nb; ++i) {
-        // lane i's view of its session state
-        const int32_t ws = __shfl_sync(0xffffffffu, aff, i);
-        const bool cached_i = (aff >= 0) && !term_lv && (Te - tend_lv <= ttl_lv);   // Alg. 1 with m = 0
-        const bool cached = __shfl_sync(0xffffffffu, cached_i, i);
-        const int64_t Lws = __shfl_sync(0xffffffffu, (long long)L, ws >= 0 ? ws : 0);
-        uint32_t w;
-        if (cached && 1000 * Lws < (int64_t)a.theta_pm * (int64_t)K * E) {
-          w = (uint32_t)ws;
-        } else {  // argmin load; ties -> lowest worker id
-          int64_t kL = act_lane ? L : INT64_MAX;
-          uint32_t kW = lane;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            int64_t oL = __shfl_xor_sync(0xffffffffu, (long long)kL, o);
-            uint32_t oW = __shfl_xor_sync(0xffffffffu, kW, o);
-            if (oL < kL || (oL == kL && oW < kW)) { kL = oL; kW = oW; }
-          }
-          w = kW;
+        const uint32_t inf = __shfl_sync(0xffffffffu, info, i);
+        int32_t ws;
+        bool cached, fin_old;
+        if (inf & (1u << 10)) {  // post-state of the latest earlier call of the session
+          const SessRec st = b_st[(inf >> 12) & 31u];
+          ws = st.aff; cached = is_cached(st); fin_old = (st.ttlf & S_FIN) != 0;
+        } else {
+          ws = (inf & 0xFFu) == 0xFFu ? -1 : (int32_t)(inf & 0xFFu);
+          cached = (inf >> 8) & 1u; fin_old = (inf >> 9) & 1u;
         }
-        const bool use_cached = cached && (int32_t)w == ws;
-        const uint32_t omega = __shfl_sync(0xffffffffu, use_cached ? pre.om_cached : pre.om_full, i);
-        const uint32_t tyi = __shfl_sync(0xffffffffu, ty, i);
-        const uint32_t si = __shfl_sync(0xffffffffu, s, i);
-        const bool fin_old = __shfl_sync(0xffffffffu, fin, i);
-        const bool f_new = __shfl_sync(0xffffffffu, f_new_l, i);
+        bool stay = false;
+        if (cached) stay = 1000 * (int64_t)__shfl_sync(0xffffffffu, (long long)L, ws) < cap_theta;
+        uint32_t w;
+        if (stay) {
+          w = (uint32_t)ws;
+        } else {  // argmin load, ties -> lowest worker id: min of (L << 5 | w), 0 <= L < 2^58
+          const uint64_t key = act_lane ? ((uint64_t)L << 5) | lane : ~0ull;
+          const uint32_t hi = (uint32_t)(key >> 32);
+          const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+          w = __reduce_min_sync(0xffffffffu, hi == mh ? (uint32_t)key : 0xFFFFFFFFu) & 31u;
+        }
+        const uint32_t c = next + i;
+        const CallRec& r = ring[(c / CH) & 1][c % CH];
         if (lane == w) {
+          const uint4 q = *reinterpret_cast<const uint4*>(&r);  // s, e, om_cached, om_full
+          const uint32_t omega = (cached && (int32_t)w == ws) ? q.z : q.w;
           if (nW >= Q) atomicOr(&errf, 1u);
           else {
             const uint32_t j = w_at(nW);
-            wS[j] = si; wR[j] = omega; ++nW;
+            wS[j] = q.x; wR[j] = omega; ++nW;
             LW += min((int64_t)omega, E);
             L += min((int64_t)omega, E);
           }
           got = true;
         }
-        if (lane == 0) {
-          if (ws >= 0 && w != (uint32_t)ws) ++reroutes;
-          if (ws >= 0 && !fin_old) cnt[ws][tyi]--;
-          if (!f_new) cnt[w][tyi]++;
+        if (lane == i) { my_w = w; my_ws = ws; my_fin = fin_old; }
+        if (inf & (1u << 11)) {  // a later call of the session in this batch reads the post-state
+          if (lane == 0) {
+            const uint32_t tyf = r.tyf;
+            b_st[i] = SessRec{(int32_t)w, r.ttl | ((tyf & F_FNEW) ? S_FIN : 0u) | ((tyf & F_TERM) ? S_TERM : 0u), r.tend};
+          }
+          __syncwarp();
         }
-        if (lane == i) a.node_of[c] = (uint8_t)w;
-        // forward the post-call state to later lanes of the same session in this batch
-        const int64_t tendi = __shfl_sync(0xffffffffu, (long long)pre.tend, i);
-        const uint32_t ttli = __shfl_sync(0xffffffffu, pre.ttl, i);
-        const bool termi = __shfl_sync(0xffffffffu, (int)((pre.tyf & F_TERM) != 0), i);
-        if (valid && (lane == i || (lane > i && ((same >> i) & 1u)))) {
-          aff = (int32_t)w; fin = f_new;
-          term_lv = termi; tend_lv = tendi; ttl_lv = ttli;
-        }
-        __syncwarp();
       }
-      // the last lane of each session in the batch publishes the session state
-      const uint32_t later = same & ~((2u << lane) - 1u);
-      if (valid && later == 0) {
-        SessRec r{aff, (uint32_t)ttl_lv | (fin ? S_FIN : 0u) | (term_lv ? S_TERM : 0u), tend_lv};
-        sess[s] = r;
+      const uint32_t ty = pre.tyf & 0xFFFFu;
+      const bool f_new = (pre.tyf & F_FNEW) != 0;
+      const bool dec = valid && my_ws >= 0 && !my_fin, inc = valid && !f_new;
+      if (dec) atomicSub(&cnt[my_ws][ty], 1);
+      if (inc) atomicAdd(&cnt[my_w][ty], 1);
+      const uint32_t rr = __popc(__ballot_sync(0xffffffffu, valid && my_ws >= 0 && my_w != (uint32_t)my_ws));
+      if (lane == 0) reroutes += rr;
+      if (valid) {
+        a.node_of[next + lane] = (uint8_t)my_w;
+        // the last call of each session in the batch publishes the session state
+        if (!has_later)
+          sess[pre.s] = SessRec{(int32_t)my_w, pre.ttl | (f_new ? S_FIN : 0u) | ((pre.tyf & F_TERM) ? S_TERM : 0u), pre.tend};
       }
       __syncwarp();
       next += nb;
@@ -387,49 +387,52 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
       load_ps();
     }
     // ---------------- act(w, a) log for nodes that received records at this boundary ----------------
-    const uint32_t gm = __ballot_sync(0xffffffffu, act_lane && got);
+    // mask(w) bit t = cnt[w][t] > 0: one ballot per node over lanes t < n_types
+    uint32_t gm = __ballot_sync(0xffffffffu, act_lane && got);
     if (gm) {
-      uint32_t mask = 0;
-      if (act_lane) for (uint32_t t2 = 0; t2 < v.n_types; ++t2) if (cnt[lane][t2] > 0) mask |= 1u << t2;
-      uint32_t base = n_act;
-      if (got) {
-        uint32_t pos = base + __popc(gm & ((1u << lane) - 1u));
-        if (pos < a.act_cap) a.act[pos] = ActRec{(uint32_t)e, lane, mask, 0u};
-        else atomicOr(&errf, 2u);
+      uint32_t pos = n_act;
+      if (pos + __popc(gm) > a.act_cap) { if (lane == 0) errf |= 2u; }
+      else {
+        for (; gm; gm &= gm - 1, ++pos) {
+          const uint32_t w = __ffs(gm) - 1;
+          const uint32_t mask = __ballot_sync(0xffffffffu, lane < v.n_types && cnt[w][lane] > 0);
+          if (lane == 0) a.act[pos] = ActRec{(uint32_t)e, w, mask, 0u};
+        }
+        if (lane == 0) n_act = pos;
       }
-      __syncwarp();
-      if (lane == 0) n_act = base + __popc(gm);
       __syncwarp();
     }
     if (errf & 1u) break;
     // ---------------- closed-form advance over service-only epochs ----------------
-    const bool all_fit = __ballot_sync(0xffffffffu, act_lane && nS + nW > K) == 0;
-    if (all_fit) {
-      const uint32_t e_next = __shfl_sync(0xffffffffu, pre.e, 0);
-      if (act_lane) admit();  // everything fits: every queued call is served each epoch
-      uint64_t k;
-      if (next >= NC) {
-        int64_t mx = (act_lane && nS) ? sF[s_at(nS - 1)] - V : 0;
-        mx = -warp_min64(-mx);
-        k = (uint64_t)ceil_div64(mx, E);
-      } else {
-        k = (uint64_t)e_next - 1 - e;
-      }
-      if (k > 0 && act_lane) {
-        const int64_t mx = nS ? sF[s_at(nS - 1)] - V : 0;  // < 2^32 (work is u32 us)
-        const bool empty = nS + nW == 0;
-        int64_t served = 0;
-        complete(V + (int64_t)k * E, V, served);
-        if (empty) idle += (int64_t)k;
-        else {
-          const uint32_t mx32 = (uint32_t)mx, E32 = (uint32_t)E;  // 0 <= mx < 2^32
-          const uint64_t m = mx32 / E32 + (mx32 % E32 != 0u);
-          idle = m >= k ? 0 : (int64_t)(k - m);
+    // When every queue fits its kappa servers, nothing happens before the next admission epoch
+    // but service: jump there in one step, including that epoch's P1.
+    if (__ballot_sync(0xffffffffu, act_lane && nS + nW > K) == 0) {
+      if (next >= NC) break;  // no arrival, no waiting call to steal: only service remains
+      const uint64_t e_next = __shfl_sync(0xffffffffu, pre.e, 0);
+      const uint64_t k = e_next - e;  // >= 1 epochs of service (the last one is e_next's P1)
+      if (act_lane) {
+        admit();  // everything fits: every queued call is served each epoch
+        if (nS == 0) {
+          idle += (int64_t)k;
+        } else {
+          // m = ceil(mx / E) epochs with service (mx = the largest remaining work, 0 < mx < 2^32);
+          // the last of the k epochs is served iff m >= k, i.e. mx > (k - 1) E
+          const int64_t mx = sF[sh + nS - 1] - V;
+          if (mx > (int64_t)(k - 1) * E) {
+            idle = 0;
+          } else {
+            const uint32_t mx32 = (uint32_t)mx, E32 = (uint32_t)E;
+            idle = (int64_t)k - (int64_t)(mx32 / E32 + (mx32 % E32 != 0u));
+          }
         }
+        complete(V + (int64_t)k * E);
         V += (int64_t)k * E;
         L = load_of();
       }
-      e += k;
+      __syncwarp();
+      e = e_next;
+      p1_done = true;
+      continue;
     }
     __syncwarp();
     ++e;
@@ -470,7 +473,7 @@ saga_status run_placement(saga_trace* t) {
   const uint32_t K = t->pcfg.kappa;
   if (K > 256) { set_error("saga_load_trace: kappa > 256 is not supported"); return SAGA_ERR_INVALID_ARG; }
   const size_t sess_bytes = ((size_t)v.n_sessions * (sizeof(SessRec) + 1) + 15) & ~(size_t)15;
-  const size_t srv_bytes = (size_t)W * K * 12;  // S: finish thresholds + sessions
+  const size_t srv_bytes = (size_t)W * 2 * K * 12;  // S: finish thresholds + sessions (2K slots)
   // sessions in shared memory if that still leaves >= 256 waiting slots per node
   const bool ss = sess_bytes + srv_bytes + 256ull * 8 * W <= max_smem;
   if (srv_bytes + 64ull * 8 * W > max_smem) { set_error("saga_load_trace: kappa x nodes too large"); return SAGA_ERR_INVALID_ARG; }
