@@ -339,6 +339,10 @@ __device__ __forceinline__ void emit_bits(uint32_t* vlist, uint32_t* n_vict, uin
   for (uint32_t y = bits; y; y &= y - 1) vlist[b0++] = (wi * 32u + (uint32_t)(__ffs(y) - 1)) | tag;
 }
 
+#ifndef SAGA_HB_BATCH
+#define SAGA_HB_BATCH 4
+#endif
+constexpr int HB_BATCH = SAGA_HB_BATCH;
 // take (clear and list) every set bit with index >= T, starting at c1 block j1 of c2 block j2
 __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, uint32_t* vlist, uint32_t* n_vict,
                              uint32_t tag) {
@@ -351,18 +355,18 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
       const uint32_t ci = i0 + lane;
       const uint32_t cv = ci < hi ? h.c1[ci] : 0u;
       uint32_t nz = __ballot_sync(0xffffffffu, cv != 0);
-      while (nz) {  // up to 4 non-empty c1 blocks at a time: their word loads are issued together
-        uint32_t c1i[4], wv[4];
+      while (nz) {  // up to HB_BATCH non-empty c1 blocks at a time: their word loads are issued together
+        uint32_t c1i[HB_BATCH], wv[HB_BATCH];
         int nb = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < HB_BATCH; ++b) {
           c1i[b] = NONE;
           if (nz) { c1i[b] = i0 + (uint32_t)(__ffs(nz) - 1); nz &= nz - 1; ++nb; }
         }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) wv[b] = c1i[b] != NONE ? h.bits[c1i[b] * 32u + lane] : 0u;
+        for (int b = 0; b < HB_BATCH; ++b) wv[b] = c1i[b] != NONE ? h.bits[c1i[b] * 32u + lane] : 0u;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < HB_BATCH; ++b) {
           if (b >= nb) break;
           const uint32_t wi = c1i[b] * 32u + lane;
           const uint32_t m = wi > tw ? 0xffffffffu : (wi == tw ? ~((1u << (T & 31)) - 1u) : 0u);
@@ -379,7 +383,9 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
 
 // take the k highest set bits (1 <= k <= total).  The threshold is found by warp 0 alone
 // (c2 level, then the 1024 c1 entries of the pivot c2 block as 32 lanes x 32, then 32 words).
-__device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t tag, Smem& sm, uint32_t* dbg) {
+// (SAGA_REPLAY_TRACE: ph / ph_t non-null -> the threshold search's cycles go to phase slot 2)
+__device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t tag, Smem& sm, uint32_t* dbg,
+                            long long* ph = nullptr, long long* ph_t = nullptr) {
   if (threadIdx.x < 32) {
     const uint32_t lane = threadIdx.x;
     if (lane == 0) sm.thr = NONE;
@@ -459,6 +465,7 @@ __device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t t
   done:;
   }
   __syncthreads();
+  if (ph && threadIdx.x == 0) { const long long t = clock64(); ph[2] += t - *ph_t; *ph_t = t; }
   if (sm.thr != NONE) hb_take_from(h, sm.hb_j2, sm.hb_j1, sm.thr, vlist, &sm.n_vict, tag);
 }
 
@@ -493,7 +500,8 @@ __device__ __forceinline__ uint32_t owner_size(const TraceView& v, const CallKey
 }
 
 // per-phase SM cycles of thread 0 (SAGA_REPLAY_TRACE): 0 updates+R1, 1 R2, 2 R3 normalisers,
-// 3 R3 keys+pivot, 4 R3 evict, 5 victims, 6 R4, 7 live list
+// 3 R3 keys+pivot, 4 R3 evict, 5 victims, 6 R4, 7 live list (BELADY / LRU: 2 = threshold
+// searches of the hierarchical bitmaps, 3 = taking every dead block)
 #define PH(i)                                                   \
   do {                                                          \
     if (a.phase_cyc && threadIdx.x == 0) {                      \
@@ -800,11 +808,12 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           const uint32_t nd_ = sm.tot_dead, np_ = sm.tot_pend - inAS;
           if (threadIdx.x == 0 && sm.tot_pend < inAS) dbg_fail(a.dbg, __LINE__, sm.tot_pend, inAS, e);
           if (k <= nd_) {
-            hb_take_top(dead, k, vlist, VT_LID, sm, a.dbg);
+            hb_take_top(dead, k, vlist, VT_LID, sm, a.dbg, a.phase_cyc ? ph : nullptr, &ph_t);
           } else {
             if (nd_ > 0) hb_take_from(dead, 0, 0, 0, vlist, &sm.n_vict, VT_LID);
             __syncthreads();
-            if (k - nd_ <= np_) hb_take_top(pend, k - nd_, vlist, 0u, sm, a.dbg);
+            PH(3);  // (BELADY: slot 3 = taking every dead block)
+            if (k - nd_ <= np_) hb_take_top(pend, k - nd_, vlist, 0u, sm, a.dbg, a.phase_cyc ? ph : nullptr, &ph_t);
             else { bad = 1; if (threadIdx.x == 0) dbg_fail(a.dbg, __LINE__, k, nd_, np_); }
           }
           __syncthreads();
@@ -814,7 +823,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           }
         } else if (lru) {
           // every resident non-in-flight block has one bit; k <= |cand| because |A| <= C
-          hb_take_top(rec, k, vlist, 0u, sm, a.dbg);
+          hb_take_top(rec, k, vlist, 0u, sm, a.dbg, a.phase_cyc ? ph : nullptr, &ph_t);
         } else {
           ListRec* L = lists[cur];
           // whole-unit eviction: list every resident latest position of unit u (warp-collective)
