@@ -157,7 +157,7 @@ struct Smem {
   uint32_t hist[H1];
   uint32_t hist2[1024];  // second-level digit histogram (cleared with hist, no extra barrier)
   uint32_t res_j, res_rem, thr, item;
-  uint32_t hb_j2, hb_j1;
+  uint32_t hb_j2, hb_j1, hb_r1;
   uint32_t n_app, n_piv, n_vict, n_vu, n_pu, pu_i;
   uint32_t ilo, ihi;
   uint32_t tot_dead, tot_pend;  // BELADY: set bits of the two hierarchical bitmaps
@@ -343,11 +343,13 @@ __device__ __forceinline__ void emit_bits(uint32_t* vlist, uint32_t* n_vict, uin
 #define SAGA_HB_BATCH 4
 #endif
 constexpr int HB_BATCH = SAGA_HB_BATCH;
-// take (clear and list) every set bit with index >= T, starting at c1 block j1 of c2 block j2
-__device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, uint32_t* vlist, uint32_t* n_vict,
+// take (clear and list) the r1 highest set bits of c1 block j1 (r1 = NONE: all of them) and every
+// set bit above that block, starting in c2 block j2.  Block j1's cut is found here from the words
+// the take loads anyway (a suffix count over the warp, lane 31 = highest word), so the threshold
+// search above stops at the c1 level and saves one dependent global round trip.
+__device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t r1, uint32_t* vlist, uint32_t* n_vict,
                              uint32_t tag) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t tw = T >> 5;
   for (uint32_t jb = j2; jb < h.n2; ++jb) {
     if (jb > j2 && h.c2[jb] == 0) continue;
     const uint32_t lo = (jb == j2) ? j1 : jb * 1024u, hi = jb * 1024u + 1024u;
@@ -369,9 +371,21 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
         for (int b = 0; b < HB_BATCH; ++b) {
           if (b >= nb) break;
           const uint32_t wi = c1i[b] * 32u + lane;
-          const uint32_t m = wi > tw ? 0xffffffffu : (wi == tw ? ~((1u << (T & 31)) - 1u) : 0u);
-          const uint32_t tk = wv[b] & m;
-          if (tk) h.bits[wi] = wv[b] & ~m;
+          uint32_t tk = wv[b];
+          if (c1i[b] == j1 && r1 != NONE) {  // keep all but the r1 highest set bits of the block
+            const uint32_t c = __popc(tk);
+            uint32_t xs = c;  // inclusive suffix count from lane 31 down
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_down_sync(0xffffffffu, xs, o);
+              if (lane + o < 32) xs += y;
+            }
+            const uint32_t above = xs - c;  // set bits in higher words of the block
+            if (above >= r1) tk = 0;
+            else if (above + c > r1)
+              for (uint32_t z = above + c - r1; z > 0; --z) tk &= tk - 1;  // the lowest bits stay
+          }
+          if (tk) h.bits[wi] = wv[b] & ~tk;
           emit_bits(vlist, n_vict, wi, tk, tag);
           const uint32_t n = warp_sum(__popc(tk));
           if (lane == 0 && n) { h.c1[c1i[b]] -= n; atomicSub(&h.c2[jb], n); }
@@ -381,8 +395,9 @@ __device__ void hb_take_from(const HB& h, uint32_t j2, uint32_t j1, uint32_t T, 
   }
 }
 
-// take the k highest set bits (1 <= k <= total).  The threshold is found by warp 0 alone
-// (c2 level, then the 1024 c1 entries of the pivot c2 block as 32 lanes x 32, then 32 words).
+// take the k highest set bits (1 <= k <= total).  The cut is found by warp 0 alone at the count
+// levels (c2, then the 1024 c1 entries of the pivot c2 block as 32 lanes x 32); hb_take_from
+// places it inside the pivot c1 block from the words it loads.
 // (SAGA_REPLAY_TRACE: ph / ph_t non-null -> the threshold search's cycles go to phase slot 2)
 __device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t tag, Smem& sm, uint32_t* dbg,
                             long long* ph = nullptr, long long* ph_t = nullptr) {
@@ -442,31 +457,13 @@ __device__ void hb_take_top(const HB& h, uint32_t k, uint32_t* vlist, uint32_t t
     }
     j1 = __shfl_sync(0xffffffffu, j1, L);
     r1 = __shfl_sync(0xffffffffu, r1, L);
-    // word level
-    const uint32_t wi = j1 * 32u + (31u - lane);  // lane 0 = highest word of the block
-    const uint32_t wv = h.bits[wi];
-    const uint32_t cw = __popc(wv);
-    uint32_t xw = cw;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, xw, o);
-      if (lane >= (uint32_t)o) xw += y;
-    }
-    if (xw - cw < r1 && r1 <= xw) {
-      uint32_t need = r1 - (xw - cw), w2 = wv;
-      int b = 31 - __clz(w2);
-      while (--need) { w2 &= ~(1u << b); b = 31 - __clz(w2); }
-      sm.thr = wi * 32u + (uint32_t)b;
-      sm.hb_j2 = j2;
-      sm.hb_j1 = j1;
-    }
-    if (!__ballot_sync(0xffffffffu, xw - cw < r1 && r1 <= xw) && lane == 0) dbg_fail(dbg, __LINE__, k, r1, j1);
+    if (lane == 0) { sm.thr = 1u; sm.hb_j2 = j2; sm.hb_j1 = j1; sm.hb_r1 = r1; }
     }
   done:;
   }
   __syncthreads();
   if (ph && threadIdx.x == 0) { const long long t = clock64(); ph[2] += t - *ph_t; *ph_t = t; }
-  if (sm.thr != NONE) hb_take_from(h, sm.hb_j2, sm.hb_j1, sm.thr, vlist, &sm.n_vict, tag);
+  if (sm.thr != NONE) hb_take_from(h, sm.hb_j2, sm.hb_j1, sm.hb_r1, vlist, &sm.n_vict, tag);
 }
 
 __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
@@ -810,7 +807,7 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
           if (k <= nd_) {
             hb_take_top(dead, k, vlist, VT_LID, sm, a.dbg, a.phase_cyc ? ph : nullptr, &ph_t);
           } else {
-            if (nd_ > 0) hb_take_from(dead, 0, 0, 0, vlist, &sm.n_vict, VT_LID);
+            if (nd_ > 0) hb_take_from(dead, 0, 0, NONE, vlist, &sm.n_vict, VT_LID);
             __syncthreads();
             PH(3);  // (BELADY: slot 3 = taking every dead block)
             if (k - nd_ <= np_) hb_take_top(pend, k - nd_, vlist, 0u, sm, a.dbg, a.phase_cyc ? ph : nullptr, &ph_t);
