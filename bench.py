@@ -379,9 +379,12 @@ def main():
     ap.add_argument("--no-bulk", action="store_true")
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
     ap.add_argument("--inflight", type=int, default=None,
-                    help="independent steps in flight on separate streams (default 2)")
+                    help="independent steps in flight on separate streams (default 3 at N=1; 2 + 2R node-sharded, <= 12)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="chain each step's expansion to the previous step's finished replay")
+    ap.add_argument("--stream-priority", type=int, default=-1,
+                    help="priority of the step streams (load, placement, expansion, sort); the library runs "
+                         "each replay kernel on its own lowest-priority stream (0: everything equal)")
     ap.add_argument("--policy-mask", type=int, default=3,
                     help="1 AEG, 2 BELADY, 4 EVICT_ALL, 8 LRU, 16 LRU+Prefix (default 3: the metric's pair)")
     args = ap.parse_args()
@@ -431,7 +434,9 @@ def main():
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
     comm = comms[0]
     p_rank, p_world = (0, 1) if trials else (rank, world)
-    streams = [torch.cuda.Stream(device=dev) for _ in range(inflight)]
+    # high-priority step streams: the next step's short kernels take SMs freed by a running replay
+    # ahead of another replay's queued CTAs, so a replay is always ready to fill the machine
+    streams = [torch.cuda.Stream(device=dev, priority=args.stream_priority) for _ in range(inflight)]
     stream = streams[0]
     host_pinned = saga.HostDesc(desc, pinned=True)
     # device-resident descriptor for `value` (the library deep-copies it device-to-device)

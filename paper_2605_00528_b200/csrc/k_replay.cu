@@ -1527,11 +1527,34 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   a.vlog = reinterpret_cast<unsigned long long*>(vlog);
   a.vlog_n = reinterpret_cast<unsigned long long*>(vlog_n);
   a.vlog_cap = vlog_cap;
-  prof_begin(SAGA_PROF_REPLAY, s);
-  k_replay<<<grid, RT, dyn, s>>>(a);
-  prof_end(SAGA_PROF_REPLAY, s);
+  // the kernel runs on the handle's lowest-priority stream, ordered after everything queued on s
+  // and before anything queued on s later (scratch stays stream-ordered on s)
+  cudaStream_t ks = s;
+  if (s && !getenv("SAGA_REPLAY_SAME_STREAM")) {
+    if (!t->replay_stream) {
+      int least = 0, greatest = 0;
+      SAGA_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      SAGA_CK(cudaStreamCreateWithPriority(&t->replay_stream, cudaStreamNonBlocking, least));
+    }
+    ks = t->replay_stream;
+    cudaEvent_t ev;
+    SAGA_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SAGA_CK(cudaEventRecord(ev, s));
+    SAGA_CK(cudaStreamWaitEvent(ks, ev, 0));
+    cudaEventDestroy(ev);
+  }
+  prof_begin(SAGA_PROF_REPLAY, ks);
+  k_replay<<<grid, RT, dyn, ks>>>(a);
+  prof_end(SAGA_PROF_REPLAY, ks);
   count_launch();
   SAGA_CK_LAUNCH();
+  if (ks != s) {
+    cudaEvent_t ev;
+    SAGA_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SAGA_CK(cudaEventRecord(ev, ks));
+    SAGA_CK(cudaStreamWaitEvent(s, ev, 0));
+    cudaEventDestroy(ev);
+  }
   // asynchronous: the scratch returns to the stream-ordered cache; the kernel's internal checks
   // land in t->replay_status and are reported by saga_replay_wait (or a synchronising call)
   std::vector<unsigned long long> cyc(trace ? 9ull * n_items : 0);

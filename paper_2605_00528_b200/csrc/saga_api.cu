@@ -254,6 +254,7 @@ void saga_free_trace(saga_trace* t) {
   cudaSetDevice(t->device);
   for (void* p : t->allocs) ws_free(p, t->stream);
   if (cudaStreamSynchronize(t->stream) == cudaSuccess) ws_release_stream(t->stream);  // reusable by other streams
+  if (t->replay_stream) cudaStreamDestroy(t->replay_stream);  // its work was joined back to t->stream
   cudaSetDevice(prev);
   delete t;
 }

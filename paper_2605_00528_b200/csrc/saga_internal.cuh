@@ -161,6 +161,10 @@ struct NodeDev {
 struct saga_trace {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // the replay kernel's own stream, at the device's lowest priority (joined to and from `stream`
+  // by events): a launch set of short kernels from other work (the next step's expansion and
+  // sort) takes SMs the replay's CTAs free before its queued replay CTAs do
+  cudaStream_t replay_stream = nullptr;
   bool sticky_error = false;
   saga_place_cfg pcfg{};
   uint32_t owned_mask = 0;
