@@ -57,7 +57,9 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms; the reported samples are those
+    taken during the timed region (begin() .. end()).  The sampler is started before the warm-up,
+    so nvidia-smi's own start-up (NVML init, ~1 s of driver work) stays out of the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -66,6 +68,7 @@ class ClockSampler:
         self.dev = dev
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -79,7 +82,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def begin(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
         if not self.proc:
@@ -92,7 +101,12 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.t0 is not None:
+            t1 = self.t1 if self.t1 is not None else float("inf")
+            inside = [x for x in lines if self.t0 <= x[0] <= t1 + 0.2]
+            lines = inside or [x for x in lines if x[0] >= self.t0][:1]
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -382,6 +396,9 @@ def main():
                     help="independent steps in flight on separate streams (default 3 at N=1; 2 + 2R node-sharded, <= 12)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="chain each step's expansion to the previous step's finished replay")
+    ap.add_argument("--gate", default="queued", choices=["queued", "none"],
+                    help="with overlap: a step's expansion starts after the previous step's replay is queued "
+                         "(queued) or right after its own placement (none)")
     ap.add_argument("--stream-priority", type=int, default=-1,
                     help="priority of the step streams (load, placement, expansion, sort); the library runs "
                          "each replay kernel on its own lowest-priority stream (0: everything equal)")
@@ -477,7 +494,8 @@ def main():
         before = after = None
         if j is not None and inflight > 1:
             def before(st):
-                if j == 0:
+                if j == 0 or (overlap and args.gate == "none"):
+                    mark(st, "go", j)
                     return
                 with order["cv"]:
                     if overlap:  # only after step j-1's replay kernel is queued (its CTAs take the SMs first)
@@ -574,6 +592,8 @@ def main():
             dist.barrier(device_ids=[local])
 
     # ---- warm-up ----
+    sampler = ClockSampler(local)
+    sampler.start()
     run_steps(max(args.warmup, inflight), dd)
     # latency of one step alone (nothing else in flight)
     lat_ms, _ = run_steps(1, dd)
@@ -596,13 +616,13 @@ def main():
     replay_accesses, n_access = int(tot[0]), int(tot[1])
 
     # ---- timed region (device-resident inputs) ----
-    sampler = ClockSampler(local)
-    sampler.start()
     l0 = saga.kernel_launches()
     barrier()
     torch.cuda.synchronize()
+    sampler.begin()
     ms, (caps, ctr) = run_steps(args.steps, dd)
     barrier()
+    sampler.end()
     launches = saga.kernel_launches() - l0
     clocks = sampler.stop()
     # per-kernel-family device times: the same steps again, one at a time, with the library's event
