@@ -396,6 +396,8 @@ def main():
                     help="independent steps in flight on separate streams (default 3 at N=1; 2 + 2R node-sharded, <= 12)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="chain each step's expansion to the previous step's finished replay")
+    ap.add_argument("--range-nccl", action="store_true",
+                    help="N > 1: all-reduce (W_lo, W_hi) with the library's NCCL communicator instead of a host (gloo) exchange")
     ap.add_argument("--gate", default="queued", choices=["queued", "none"],
                     help="with overlap: a step's expansion starts after the previous step's replay is queued "
                          "(queued) or right after its own placement (none)")
@@ -449,6 +451,20 @@ def main():
     inflight = min(inflight, 12)
     # one stream, trace handle and communicator per in-flight step (see run_steps)
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
+    # (W_lo, W_hi) max over ranks as a host exchange (gloo, one group per step stream): the two values
+    # are host-side after saga_sweep_range, and an NCCL kernel would wait for an SM held by replays
+    range_groups = [dist.new_group(backend="gloo") for _ in range(inflight)] \
+        if world > 1 and not args.range_nccl else [None] * inflight
+
+    def range_reduce_for(i):
+        if range_groups[i] is None:
+            return None
+
+        def red(wlo, whi):
+            x = torch.tensor([wlo, whi], dtype=torch.int64)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX, group=range_groups[i])
+            return int(x[0]), int(x[1])
+        return red
     comm = comms[0]
     p_rank, p_world = (0, 1) if trials else (rank, world)
     # high-priority step streams: the next step's short kernels take SMs freed by a running replay
@@ -525,7 +541,8 @@ def main():
                                              counters=counters[i], shard_caps=shard_caps,
                                              before_expand=before, after_replay=after,
                                              mark=(lambda st, w: mark(st, w, j)) if timeline is not None else None,
-                                             range_comm=comms[i] if trials else None, replay_wait=False)
+                                             range_comm=comms[i] if trials else None, replay_wait=False,
+                                             range_host_reduce=range_reduce_for(i))
             if trials and comms[i] is not None:  # A8: combine the per-trial counters over ranks
                 comms[i].allreduce(ctr, op=0, stream=t.stream)
         counters[i] = ctr

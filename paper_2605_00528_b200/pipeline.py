@@ -17,9 +17,13 @@ def owned_nodes(n_nodes: int, rank: int, world: int):
 
 def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, world: int = 1, comm=None,
              device: int = 0, stream=None, host=None, counters=None, shard_caps: bool = False,
-             before_expand=None, after_replay=None, mark=None, range_comm=None, replay_wait: bool = True):
+             before_expand=None, after_replay=None, mark=None, range_comm=None, replay_wait: bool = True,
+             range_host_reduce=None):
     """Returns (trace handle, caps list, counters tensor [n_pol, n_caps, n_nodes, 16]).
 
+    range_host_reduce(wlo, whi) -> (wlo, whi), when given, replaces the NCCL max all-reduce of
+    (W_lo, W_hi): the values are already on the host (saga_sweep_range synchronises), and an NCCL
+    kernel would have to wait for an SM that the replays in flight hold for 100+ ms.
     before_expand(stream), when given, defers A3 (SAGA_LOAD_DEFER_EXPAND) and is called between
     placement and the first expansion; after_replay(stream) is called after the replay launch.
     bench.py uses them to keep one step's expansion/next-use/replay behind the previous step's
@@ -43,7 +47,9 @@ def run_step(desc, place_cfg: dict, replay_cfg: dict, caps_fn, rank: int = 0, wo
         a, b = t.sweep_range(w)
         wlo, whi = max(wlo, a), max(whi, b)
     rcomm = comm if (comm is not None and world > 1) else range_comm
-    if rcomm is not None:  # A8 #1 (range_comm: independent trials that still share one sweep)
+    if range_host_reduce is not None:  # A8 #1 as a host exchange of the two host-side values
+        wlo, whi = range_host_reduce(wlo, whi)
+    elif rcomm is not None:  # A8 #1 (range_comm: independent trials that still share one sweep)
         rng = torch.tensor([wlo, whi], dtype=torch.int64, device=f"cuda:{device}")
         rcomm.allreduce(rng, op=1, stream=t.stream)
         t.stream.synchronize()
