@@ -912,6 +912,9 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
               if (vic) vunits[b0 + __popc(vm & ((1u << lane) - 1u))] = i;
             }
             __syncthreads();
+#ifdef SAGA_TRACE_SPLIT4
+            PH(7);  // (experiment: pass c's cycles into slot 7)
+#endif
             const uint32_t nvu = sm.n_vu;
             // one pivot unit whose local ids increase with position: its r2 largest lids are its
             // r2 highest resident positions -- no ranking needed
