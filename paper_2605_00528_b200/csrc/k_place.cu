@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   off += (size_t)W * Q * 4;
   uint32_t* wR = reinterpret_cast<uint32_t*>(smem_raw + off) + (size_t)lane * Q;   // W: work (us)
   __shared__ int32_t cnt[32][32];                       // sessions with aff = w, !fin, by type
+  __shared__ uint32_t amask[32];                        // bit t of node w: cnt[w][t] > 0 (the act mask)
   __shared__ __align__(16) SessRec b_st[32];            // P3 batch: post-state of call next + i
   // call records streamed ahead by TMA bulk copies: chunk j (calls [256 j, 256 j + 256)) lives
   // in buffer j & 1; chunk j + 1 is requested when chunk j is first touched
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
   __shared__ uint32_t xfer_n, n_mig, n_act, errf;
   __shared__ unsigned long long steals, reroutes;
   for (int i = lane; i < 32 * 32; i += 32) (&cnt[0][0])[i] = 0;
+  amask[lane] = 0;
   if (SS) {
     const SessRec init{-1, 0u, 0ll};
     for (uint32_t i = lane; i < NS; i += 32) { sess[i] = init; moved[i] = 0; }
@@ -282,8 +284,9 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           SessRec sr = sess[s];
           const uint32_t ty = v.styp[s];
           if (!(sr.ttlf & S_FIN)) {  // s is counted at its current affinity node
-            cnt[sr.aff][ty]--;
-            cnt[th][ty]++;
+            const int32_t xa = --cnt[sr.aff][ty], xt = ++cnt[th][ty];
+            amask[sr.aff] = xa > 0 ? (amask[sr.aff] | (1u << ty)) : (amask[sr.aff] & ~(1u << ty));
+            amask[th] = xt > 0 ? (amask[th] | (1u << ty)) : (amask[th] & ~(1u << ty));
           }
           sr.aff = (int32_t)th;
           sess[s] = sr;
@@ -304,8 +307,8 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
     // session state; the calls are then routed in order, every lane following call i uniformly
     // (one shuffle of lane i's packed view, the stay test, a two-step redux argmin).  A call whose
     // session already had a call earlier in the batch reads that call's post-state from b_st.
-    // The affinity counts, reroute count and session records are updated per batch, in
-    // parallel, after the routing.
+    // The affinity counts (and act-mask bits), reroute count and session records are updated per
+    // batch, in parallel, after the routing.
     while (next < NC && __shfl_sync(0xffffffffu, pre.e, 0) == (uint32_t)e) {
       const bool valid = next + lane < NC && pre.e == (uint32_t)e;
       const uint32_t nb = __popc(__ballot_sync(0xffffffffu, valid));
@@ -381,25 +384,27 @@ __global__ void __launch_bounds__(32, 1) k_place(PlaceArgs a) {
           sess[pre.s] = SessRec{(int32_t)my_w, pre.ttl | (f_new ? S_FIN : 0u) | ((pre.tyf & F_TERM) ? S_TERM : 0u), pre.tend};
       }
       __syncwarp();
+      // act-mask bits of the (node, type) counts this batch touched: every lane sees the final count
+      if (dec) { if (cnt[my_ws][ty] > 0) atomicOr(&amask[my_ws], 1u << ty); else atomicAnd(&amask[my_ws], ~(1u << ty)); }
+      if (inc) { if (cnt[my_w][ty] > 0) atomicOr(&amask[my_w], 1u << ty); else atomicAnd(&amask[my_w], ~(1u << ty)); }
+      __syncwarp();
       next += nb;
       load_pre();
       __syncwarp();
       load_ps();
     }
     // ---------------- act(w, a) log for nodes that received records at this boundary ----------------
-    // mask(w) bit t = cnt[w][t] > 0: one ballot per node over lanes t < n_types
-    uint32_t gm = __ballot_sync(0xffffffffu, act_lane && got);
+    // mask(w) = amask[w], kept up to date with the counts (bit t: cnt[w][t] > 0)
+    const uint32_t gm = __ballot_sync(0xffffffffu, act_lane && got);
     if (gm) {
-      uint32_t pos = n_act;
-      if (pos + __popc(gm) > a.act_cap) { if (lane == 0) errf |= 2u; }
-      else {
-        for (; gm; gm &= gm - 1, ++pos) {
-          const uint32_t w = __ffs(gm) - 1;
-          const uint32_t mask = __ballot_sync(0xffffffffu, lane < v.n_types && cnt[w][lane] > 0);
-          if (lane == 0) a.act[pos] = ActRec{(uint32_t)e, w, mask, 0u};
-        }
-        if (lane == 0) n_act = pos;
+      const uint32_t base = n_act;
+      if (got) {
+        const uint32_t pos = base + __popc(gm & ((1u << lane) - 1u));
+        if (pos < a.act_cap) a.act[pos] = ActRec{(uint32_t)e, lane, amask[lane], 0u};
+        else atomicOr(&errf, 2u);
       }
+      __syncwarp();
+      if (lane == 0) n_act = base + __popc(gm);
       __syncwarp();
     }
     if (errf & 1u) break;

@@ -499,6 +499,7 @@ __device__ __forceinline__ uint32_t owner_size(const TraceView& v, const CallKey
 // per-phase SM cycles of thread 0 (SAGA_REPLAY_TRACE): 0 updates+R1, 1 R2, 2 R3 normalisers,
 // 3 R3 keys+pivot, 4 R3 evict, 5 victims, 6 R4, 7 live list (BELADY / LRU: 2 = threshold
 // searches of the hierarchical bitmaps, 3 = taking every dead block)
+#ifndef SAGA_TRACE_COUNT_PIVOT
 #define PH(i)                                                   \
   do {                                                          \
     if (a.phase_cyc && threadIdx.x == 0) {                      \
@@ -507,6 +508,16 @@ __device__ __forceinline__ uint32_t owner_size(const TraceView& v, const CallKey
       ph_t = _n;                                                \
     }                                                           \
   } while (0)
+#else  // (experiment: slots 0 / 5 / 6 count AEG eviction epochs by pivot path instead of cycles)
+#define PH(i)                                                   \
+  do {                                                          \
+    if (a.phase_cyc && threadIdx.x == 0) {                      \
+      const long long _n = clock64();                           \
+      if ((i) != 0 && (i) != 5 && (i) != 6) ph[i] += _n - ph_t; \
+      ph_t = _n;                                                \
+    }                                                           \
+  } while (0)
+#endif
 
 constexpr uint32_t VT_LID = 0x80000000u;  // victim-list tag: the entry is a local id, else a position
 #ifndef SAGA_REPLAY_UNR
@@ -973,6 +984,9 @@ __global__ void __launch_bounds__(RT, SAGA_REPLAY_MINB) k_replay(ReplayArgs a) {
             __syncthreads();
             const uint32_t npv = sm.n_piv;
             if (threadIdx.x == 0 && npv > C) dbg_fail(a.dbg, __LINE__, npv, C, r2);
+#ifdef SAGA_TRACE_COUNT_PIVOT
+            if (threadIdx.x == 0) ph[whole ? 0 : (mono_piv ? 5 : 6)] += 1000000ll;
+#endif
             if (!whole && !mono_piv && npv) {
               // pivot keys differ only in lid: rank (lid << 32 | slot) and keep the top r2
               uint32_t* pslot = vlist + k;  // (unit, position) of gathered slot i, after the list
