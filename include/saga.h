@@ -274,8 +274,11 @@ saga_status saga_evict_select(const uint64_t* key_dev, const uint64_t* seg_off_d
  * SAGA_ERR_CAPACITY if a capacity is below the block count of a single call (or
  * migration / prefetch group) at a replayed node (S:209 CapacityError).  Stream-ordered and asynchronous once the node's replay
  * index exists (the first call for a node builds it and syncs for its sizes); the kernel's
- * internal invariant checks are reported by saga_replay_wait.  Set SAGA_REPLAY_TRACE=1 to print
- * per-item / per-phase SM cycles to stderr (syncs). */
+ * internal invariant checks are reported by saga_replay_wait.  The replay kernel itself runs on a
+ * stream the handle owns, at the device's lowest priority, event-joined after the work queued on
+ * the handle's stream and before any work queued there later (ordering is unchanged; other
+ * streams' short kernels take freed SMs first; SAGA_REPLAY_SAME_STREAM=1 keeps it on the handle's
+ * stream).  Set SAGA_REPLAY_TRACE=1 to print per-item / per-phase SM cycles to stderr (syncs). */
 saga_status saga_replay(saga_trace* t, const saga_replay_cfg* cfg, const uint32_t* caps, uint32_t n_caps,
                         const uint32_t* nodes, uint32_t n_owned, int64_t* counters_dev, saga_stream_t stream);
 
