@@ -394,6 +394,8 @@ def main():
     ap.add_argument("--shard", default=None, choices=["trials", "nodes"])
     ap.add_argument("--inflight", type=int, default=None,
                     help="independent steps in flight on separate streams (default 3 at N=1; 2 + 2R node-sharded, <= 12)")
+    ap.add_argument("--overlap", action="store_true",
+                    help="overlap steps even above the default size threshold (keeps inflight expanded traces resident)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="chain each step's expansion to the previous step's finished replay")
     ap.add_argument("--range-nccl", action="store_true",
@@ -441,13 +443,17 @@ def main():
     shard_caps = (not trials) and desc.n_nodes == 1 and world > 1
     # Steps in flight.  "overlap": a step's expansion / next use start as soon as the previous
     # step's replay kernel is queued (they fill the SMs its short items free), which
-    # keeps up to inflight expanded traces resident -- only when they fit (C1-C3); larger
-    # configs chain a step's expansion to the previous step's freed trace.
-    overlap = desc.n_accesses < 3 * 10 ** 8 and not args.no_overlap
+    # keeps up to inflight expanded traces resident -- only when they fit in ~60 % of the device
+    # memory at ~48 B per owned access (node arrays + sort scratch): C1-C4; C5 chains a step's
+    # expansion to the previous step's freed trace.
     # node-sharded ranks hold 1/R of the replay items but the same per-step placement and critical
     # path (one item's epoch chain), so more steps are kept in flight as R grows
     # (latency of one step ~ 2.4x a rank's SM-time per step at C2 when R ranks split the items)
-    inflight = max(1, args.inflight or (((3 if world == 1 or shard != "nodes" else 2 + 2 * world)) if overlap else 2))
+    n_over = min(12, 3 if world == 1 or shard != "nodes" else 2 + 2 * world)
+    owned_acc = desc.n_accesses / (world if shard == "nodes" and world > 1 else 1)
+    fits = n_over * 48 * owned_acc < 0.6 * torch.cuda.get_device_properties(dev).total_memory
+    overlap = (fits or args.overlap) and not args.no_overlap
+    inflight = max(1, args.inflight or (n_over if overlap else 2))
     inflight = min(inflight, 12)
     # one stream, trace handle and communicator per in-flight step (see run_steps)
     comms = [saga.Comm(rank, world, local) for _ in range(inflight)] if world > 1 else [None] * inflight
