@@ -441,10 +441,15 @@ saga_status next_use_batch(saga_trace* t, const std::vector<uint32_t>& ws, cudaS
   SAGA_CK(d2h(hs.data(), small, 4 * 3 * MAXN, s));
   SAGA_CK(cudaStreamSynchronize(s));
   const uint32_t nc = v.n_calls;
-  uint32_t *present = nullptr, *flag = nullptr, *pos = nullptr;
+  // update lists of all nodes of the batch: kernels for every node first, then ONE host read of
+  // their lengths (each host sync waits for SMs that replays in flight may hold)
+  uint32_t* present = nullptr;
+  std::vector<uint32_t*> flag(nb, nullptr), pos(nb, nullptr);
   SAGA_CK(ws_malloc((void**)&present, (size_t(v.n_sessions) / 32 + 1) * 4, s));
-  SAGA_CK(ws_malloc((void**)&flag, (size_t(nc) + 1) * 4, s));
-  SAGA_CK(ws_malloc((void**)&pos, (size_t(nc) + 1) * 4, s));
+  for (uint32_t i = 0; i < nb; ++i) {
+    SAGA_CK(ws_malloc((void**)&flag[i], (size_t(nc) + 1) * 4, s));
+    SAGA_CK(ws_malloc((void**)&pos[i], (size_t(nc) + 1) * 4, s));
+  }
   for (uint32_t i = 0; i < nb; ++i) {
     NodeDev& nd = t->nodes[ws[i]];
     nd.w_lo = hs[2 * i];
@@ -459,22 +464,27 @@ saga_status next_use_batch(saga_trace* t, const std::vector<uint32_t>& ws, cudaS
     // update list: calls of the sessions that own a block at this node (replay session state)
     SAGA_CK(cudaMemsetAsync(present, 0, (size_t(v.n_sessions) / 32 + 1) * 4, s));
     k_present<<<grid_for(hn), NTHREADS, 0, s>>>(nd.lown, hn, v.n_sessions, present);
-    k_flag_present<<<grid_for(nc), NTHREADS, 0, s>>>(v.call_sess, nc, present, flag);
+    k_flag_present<<<grid_for(nc), NTHREADS, 0, s>>>(v.call_sess, nc, present, flag[i]);
     count_launch(2);
-    SAGA_CK(scan_u32(t, flag, pos, nc));
-    uint32_t nu = 0;
-    SAGA_CK(d2h(&nu, pos + nc, 4, s));
+    SAGA_CK(scan_u32(t, flag[i], pos[i], nc));
+    SAGA_CK(cudaMemcpyAsync(small + i, pos[i] + nc, 4, cudaMemcpyDeviceToDevice, s));  // (small is free again)
+  }
+  SAGA_CK(d2h(hs.data(), small, 4 * nb, s));
+  for (uint32_t i = 0; i < nb; ++i) {
+    NodeDev& nd = t->nodes[ws[i]];
+    const uint32_t nu = hs[i];
     nd.n_upd = nu;
     nd.upd_c = dalloc<uint32_t>(t, nu);
     if (!nd.upd_c) { set_error("out of device memory (next use)"); return SAGA_ERR_OOM; }
-    k_scatter_flag2<<<grid_for(nc), NTHREADS, 0, s>>>(flag, pos, nc, nd.upd_c);
+    k_scatter_flag2<<<grid_for(nc), NTHREADS, 0, s>>>(flag[i], pos[i], nc, nd.upd_c);
     count_launch();
     SAGA_CK_LAUNCH();
     nd.nu_done = true;
   }
   ws_free(skey, s); ws_free(sval, s); ws_free(lown, s); ws_free(l2g, s);
   ws_free(status, s); ws_free(tctr, s); ws_free(small, s); ws_free(ev_pos, s); ws_free(cnt, s);
-  ws_free(present, s); ws_free(flag, s); ws_free(pos, s);
+  ws_free(present, s);
+  for (uint32_t i = 0; i < nb; ++i) { ws_free(flag[i], s); ws_free(pos[i], s); }
   return SAGA_OK;
 }
 

@@ -1293,19 +1293,23 @@ unsigned grid_for(uint64_t n, int threads = NTHREADS) {
   return (unsigned)g;
 }
 
-saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
+// The replay index of a node, in two phases so that the index of every node of a launch needs
+// ONE host read of the sizes (each host sync waits for SMs the replays in flight may hold):
+// phase A launches the unit-head scans and copies their totals to `cnt2` on the device; phase B,
+// after the caller read them, sizes and fills the unit tables.
+struct IndexScratch { uint32_t *head = nullptr, *hpos = nullptr, *sflag = nullptr, *s2lo = nullptr; };
+
+saga_status replay_index_a(saga_trace* t, uint32_t w, cudaStream_t s, IndexScratch& x, uint32_t* cnt2) {
   NodeDev& nd = t->nodes[w];
-  if (nd.rp_done) return SAGA_OK;
   const TraceView& v = t->v;
   const uint64_t N = nd.N;
   const uint32_t J = nd.J;
   const uint32_t NS = std::max(v.n_sessions, 1u);
-  uint32_t *head = nullptr, *hpos = nullptr, *u_kind = nullptr, *u_pos = nullptr, *sflag = nullptr, *s2lo = nullptr;
-  SAGA_CK(ws_malloc((void**)&head, (N + 1) * 4, s));
-  SAGA_CK(ws_malloc((void**)&hpos, (N + 2) * 4, s));
-  SAGA_CK(ws_malloc((void**)&sflag, (size_t(NS) + 1) * 4, s));
-  SAGA_CK(ws_malloc((void**)&s2lo, (size_t(NS) + 1) * 4, s));
-  SAGA_CK(cudaMemsetAsync(sflag, 0, (size_t(NS) + 1) * 4, s));
+  SAGA_CK(ws_malloc((void**)&x.head, (N + 1) * 4, s));
+  SAGA_CK(ws_malloc((void**)&x.hpos, (N + 2) * 4, s));
+  SAGA_CK(ws_malloc((void**)&x.sflag, (size_t(NS) + 1) * 4, s));
+  SAGA_CK(ws_malloc((void**)&x.s2lo, (size_t(NS) + 1) * 4, s));
+  SAGA_CK(cudaMemsetAsync(x.sflag, 0, (size_t(NS) + 1) * 4, s));
   nd.ev_pos = dalloc<uint64_t>(t, size_t(J) + 1);
   nd.u_of = dalloc<uint32_t>(t, N);
   nd.upu = dalloc<uint32_t>(t, N);
@@ -1314,20 +1318,27 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   k_ev_pos<<<grid_for(size_t(J) + 1), NTHREADS, 0, s>>>(nd.g_pos, nd.ev_g, J, nd.ev_pos);
   count_launch();
   if (nd.n_local) {
-    k_owner_flag<<<grid_for(nd.n_local), NTHREADS, 0, s>>>(nd.lown, nd.n_local, v.n_sessions, sflag);
+    k_owner_flag<<<grid_for(nd.n_local), NTHREADS, 0, s>>>(nd.lown, nd.n_local, v.n_sessions, x.sflag);
     count_launch();
   }
-  SAGA_CK(scan_u32(t, sflag, s2lo, NS));
+  SAGA_CK(scan_u32(t, x.sflag, x.s2lo, NS));
   if (N > 0) {
-    k_unit_head<<<grid_for(N), NTHREADS, 0, s>>>(nd.lidf, nd.lown, N, head);
-    if (nd.G) k_group_head<<<grid_for(nd.G), NTHREADS, 0, s>>>(nd.g_pos, nd.G, head);
+    k_unit_head<<<grid_for(N), NTHREADS, 0, s>>>(nd.lidf, nd.lown, N, x.head);
+    if (nd.G) k_group_head<<<grid_for(nd.G), NTHREADS, 0, s>>>(nd.g_pos, nd.G, x.head);
     count_launch(2);
   }
-  SAGA_CK(scan_u32(t, head, hpos, N));
-  uint32_t hv[2] = {0, 0};
-  SAGA_CK(d2h(&hv[0], hpos + N, 4, s));
-  SAGA_CK(d2h(&hv[1], s2lo + NS, 4, s));
-  SAGA_CK(cudaStreamSynchronize(s));
+  SAGA_CK(scan_u32(t, x.head, x.hpos, N));
+  SAGA_CK(cudaMemcpyAsync(cnt2, x.hpos + N, 4, cudaMemcpyDeviceToDevice, s));
+  SAGA_CK(cudaMemcpyAsync(cnt2 + 1, x.s2lo + NS, 4, cudaMemcpyDeviceToDevice, s));
+  return SAGA_OK;
+}
+
+saga_status replay_index_b(saga_trace* t, uint32_t w, cudaStream_t s, IndexScratch& x, const uint32_t* hv) {
+  NodeDev& nd = t->nodes[w];
+  const TraceView& v = t->v;
+  const uint64_t N = nd.N;
+  const uint32_t J = nd.J;
+  uint32_t *u_kind = nullptr, *u_pos = nullptr;
   const uint32_t nu = hv[0];
   if (nu >= (1u << 29)) { set_error("node %u has %u units (limit 2^29)", w, nu); return SAGA_ERR_STATE; }
   nd.n_units = nu;
@@ -1341,26 +1352,45 @@ saga_status build_replay_index(saga_trace* t, uint32_t w, cudaStream_t s) {
   if (!nd.urec || !nd.ev_unit || !nd.ev_upd || !nd.upd_lo) { set_error("out of device memory (replay index)"); return SAGA_ERR_OOM; }
   if (N > 0) {
     UnitRec* ur = static_cast<UnitRec*>(nd.urec);
-    k_unit_fill<<<grid_for(N), NTHREADS, 0, s>>>(head, hpos, N, nd.lidf, nd.lown, nd.g_pos, nd.G, nd.g_t, nd.g_kind, s2lo,
-                                                 v.n_sessions, u_pos, ur, u_kind);
+    k_unit_fill<<<grid_for(N), NTHREADS, 0, s>>>(x.head, x.hpos, N, nd.lidf, nd.lown, nd.g_pos, nd.G, nd.g_t, nd.g_kind,
+                                                 x.s2lo, v.n_sessions, u_pos, ur, u_kind);
     k_unit_end<<<grid_for(nu), NTHREADS, 0, s>>>(u_pos, nu, N, ur);
-    k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(hpos, N, u_kind, ur, nd.u_of);
+    k_unit_of<<<grid_for(N), NTHREADS, 0, s>>>(x.hpos, N, u_kind, ur, nd.u_of);
     k_prev_unit<<<grid_for(N), NTHREADS, 0, s>>>(nd.prv, nd.u_of, N, nd.upu);
     k_unit_mono<<<grid_for(N), NTHREADS, 0, s>>>(nd.lidf, nd.u_of, N, ur);
     count_launch(5);
   }
   k_ev_index<<<grid_for(std::max<size_t>(size_t(J) + 1, nd.n_upd)), NTHREADS, 0, s>>>(
-      v, nd.ev_pos, nd.ev_e, J, hpos, N, nu, nd.upd_c, nd.n_upd, s2lo, nd.ev_unit, nd.ev_upd, nd.upd_lo);
+      v, nd.ev_pos, nd.ev_e, J, x.hpos, N, nu, nd.upd_c, nd.n_upd, x.s2lo, nd.ev_unit, nd.ev_upd, nd.upd_lo);
   count_launch();
   SAGA_CK_LAUNCH();
-  ws_free(head, s);
-  ws_free(hpos, s);
+  ws_free(x.head, s);
+  ws_free(x.hpos, s);
   ws_free(u_kind, s);
   ws_free(u_pos, s);
-  ws_free(sflag, s);
-  ws_free(s2lo, s);
+  ws_free(x.sflag, s);
+  ws_free(x.s2lo, s);
+  x = IndexScratch{};
   nd.rp_done = true;
   return SAGA_OK;
+}
+
+// the replay index of every listed node that lacks one: phase A for all, one host read, phase B
+saga_status build_replay_indices(saga_trace* t, const uint32_t* nodes, uint32_t n, cudaStream_t s) {
+  std::vector<uint32_t> todo;
+  for (uint32_t i = 0; i < n; ++i)
+    if (!t->nodes[nodes[i]].rp_done && std::find(todo.begin(), todo.end(), nodes[i]) == todo.end()) todo.push_back(nodes[i]);
+  if (todo.empty()) return SAGA_OK;
+  std::vector<IndexScratch> xs(todo.size());
+  uint32_t* cnt = nullptr;
+  SAGA_CK(ws_malloc((void**)&cnt, 8 * todo.size(), s));
+  saga_status st = SAGA_OK;
+  for (size_t i = 0; i < todo.size() && st == SAGA_OK; ++i) st = replay_index_a(t, todo[i], s, xs[i], cnt + 2 * i);
+  std::vector<uint32_t> hv(2 * todo.size());
+  if (st == SAGA_OK && d2h(hv.data(), cnt, 8 * todo.size(), s) != cudaSuccess) { set_error("replay index: %s", "d2h"); st = SAGA_ERR_CUDA; }
+  for (size_t i = 0; i < todo.size() && st == SAGA_OK; ++i) st = replay_index_b(t, todo[i], s, xs[i], &hv[2 * i]);
+  ws_free(cnt, s);
+  return st;
 }
 
 }  // namespace
@@ -1392,9 +1422,11 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
     }
   }
   uint64_t max_local = 1, maxN = 1, max_units = 1, max_lo = 1;
-  for (uint32_t i = 0; i < n_owned; ++i) {
-    saga_status st = build_replay_index(t, nodes[i], s);
+  {
+    const saga_status st = build_replay_indices(t, nodes, n_owned, s);
     if (st != SAGA_OK) return st;
+  }
+  for (uint32_t i = 0; i < n_owned; ++i) {
     const NodeDev& nd = t->nodes[nodes[i]];
     max_local = std::max<uint64_t>(max_local, nd.n_local);
     maxN = std::max<uint64_t>(maxN, nd.N);
@@ -1512,10 +1544,17 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   uint32_t *d_caps = nullptr, *d_list = nullptr, *d_items = nullptr, *work = nullptr;
   unsigned long long* d_cyc = nullptr;
   uint8_t* scratch = nullptr;
-  SAGA_CK(ws_malloc((void**)&d_nodes, sizeof(NodeArr) * t->n_nodes, s));
-  SAGA_CK(ws_malloc((void**)&d_caps, 4 * n_caps, s));
-  SAGA_CK(ws_malloc((void**)&d_list, 4 * n_owned, s));
-  SAGA_CK(ws_malloc((void**)&d_items, 4 * n_items, s));
+  // the launch's parameter arrays in one block, copied by one h2d (each copy syncs the stream)
+  const size_t o_caps = (sizeof(NodeArr) * t->n_nodes + 15) & ~size_t(15);
+  const size_t o_list = o_caps + ((4 * size_t(n_caps) + 15) & ~size_t(15));
+  const size_t o_items = o_list + ((4 * size_t(n_owned) + 15) & ~size_t(15));
+  const size_t par_bytes = o_items + 4 * size_t(n_items);
+  uint8_t* d_par = nullptr;
+  SAGA_CK(ws_malloc((void**)&d_par, par_bytes, s));
+  d_nodes = reinterpret_cast<NodeArr*>(d_par);
+  d_caps = reinterpret_cast<uint32_t*>(d_par + o_caps);
+  d_list = reinterpret_cast<uint32_t*>(d_par + o_list);
+  d_items = reinterpret_cast<uint32_t*>(d_par + o_items);
   SAGA_CK(ws_malloc((void**)&work, 32, s));
   if (!t->replay_status) {  // [0] error flag, [1..4] first failed invariant (checked by saga_replay_wait)
     t->replay_status = dalloc<uint32_t>(t, 8);
@@ -1527,10 +1566,14 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
     set_error("out of device memory (replay scratch %llu bytes)", (unsigned long long)(a.cta_bytes * grid));
     return SAGA_ERR_OOM;
   }
-  SAGA_CK(h2d(d_nodes, hn.data(), sizeof(NodeArr) * t->n_nodes, s));
-  SAGA_CK(h2d(d_caps, caps, 4 * n_caps, s));
-  SAGA_CK(h2d(d_list, nodes, 4 * n_owned, s));
-  SAGA_CK(h2d(d_items, items.data(), 4 * n_items, s));
+  {
+    std::vector<uint8_t> hp(par_bytes, 0);
+    memcpy(hp.data(), hn.data(), sizeof(NodeArr) * t->n_nodes);
+    memcpy(hp.data() + o_caps, caps, 4 * size_t(n_caps));
+    memcpy(hp.data() + o_list, nodes, 4 * size_t(n_owned));
+    memcpy(hp.data() + o_items, items.data(), 4 * size_t(n_items));
+    SAGA_CK(h2d(d_par, hp.data(), par_bytes, s));
+  }
   SAGA_CK(cudaMemsetAsync(work, 0, 32, s));
   a.v = v;
   a.nodes = d_nodes; a.caps = d_caps; a.items = d_items; a.n_items = n_items; a.node_list = d_list;
@@ -1576,7 +1619,7 @@ saga_status SAGA_REPLAY_ENTRY(saga_trace* t, const saga_replay_cfg* cfg, const u
   // land in t->replay_status and are reported by saga_replay_wait (or a synchronising call)
   std::vector<unsigned long long> cyc(trace ? 9ull * n_items : 0);
   if (trace) SAGA_CK(d2h(cyc.data(), d_cyc, 8ull * 9 * n_items, s));
-  ws_free(d_nodes, s); ws_free(d_caps, s); ws_free(d_list, s); ws_free(d_items, s);
+  ws_free(d_par, s);
   ws_free(scratch, s);
   ws_free(work, s);
   if (d_cyc) ws_free(d_cyc, s);

@@ -161,10 +161,11 @@ void give(void* p) {
 }
 }  // namespace bounce_detail
 
+// (stream-ordered copy + one sync: the copy waits for the work queued before it on s)
 cudaError_t d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
   using namespace bounce_detail;
-  cudaError_t e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess || n == 0) return e;
+  cudaError_t e = cudaSuccess;
+  if (n == 0) return cudaStreamSynchronize(s);
   void* b = n <= kBounce ? take() : nullptr;
   if ((e = cudaMemcpyAsync(b ? b : dst, src, n, cudaMemcpyDeviceToHost, s)) == cudaSuccess) e = cudaStreamSynchronize(s);
   if (b) {
@@ -176,8 +177,8 @@ cudaError_t d2h(void* dst, const void* src, size_t n, cudaStream_t s) {
 
 cudaError_t h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
   using namespace bounce_detail;
-  cudaError_t e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess || n == 0) return e;
+  cudaError_t e = cudaSuccess;
+  if (n == 0) return cudaStreamSynchronize(s);
   void* b = n <= kBounce ? take() : nullptr;
   if (b) memcpy(b, src, n);
   if ((e = cudaMemcpyAsync(dst, b ? b : src, n, cudaMemcpyHostToDevice, s)) == cudaSuccess) e = cudaStreamSynchronize(s);
